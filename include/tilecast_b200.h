@@ -1,0 +1,199 @@
+/*
+ * tilecast_b200.h -- C ABI of the B200-native batched environment step.
+ *
+ * This is the drop-in boundary for the reference's kernel plugin interface
+ * (/root/reference/pkg/src/tilecast/backend/__init__.py:28-57 selects a
+ * module exporting BACKEND_NAME / cast_ray / render_into / batch_kernel;
+ * tables.py:251-266 is the one spelling of batch_kernel's argument order).
+ * Every entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - Plain C types only: pointers, sizes, int status codes. No torch types.
+ *   - "dev" pointers are CUDA device pointers (any allocator: torch, cudaMalloc);
+ *     "host" pointers are ordinary host memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Functions return TC_OK (0) or a negative TC_E* error code; a message for
+ *     the last error on the calling thread is available via tc_last_error().
+ *   - Per-environment engine faults are NOT errors of the call: they are
+ *     written as status codes (TC_ST_*) into out->statuses, exactly like the
+ *     reference (tables.py:267-272 turns them into RuntimeError host-side).
+ *   - The library never allocates on the step path; the caller owns every
+ *     state/output buffer (tables.py:187-245 ownership rules).
+ */
+#ifndef TILECAST_B200_H
+#define TILECAST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TC_ABI_VERSION 1
+
+/* ---- call status (return values) -------------------------------------- */
+#define TC_OK 0
+#define TC_E_INVALID (-1)   /* bad argument / contract violation            */
+#define TC_E_CUDA (-2)      /* CUDA runtime error (message in tc_last_error) */
+#define TC_E_CAPACITY (-3)  /* exceeds MAX_ENTITIES / MAX_DOORS / obs size   */
+
+/* ---- per-env kernel status codes (backend/layout.py:47-51) ------------- */
+#define TC_ST_OK 0
+#define TC_ST_ESCAPED 1      /* ray left the grid: map not sealed          */
+#define TC_ST_STEP_BUDGET 2  /* ray exceeded 2*(w+h) boundary steps        */
+#define TC_ST_BAD_ACTION 3   /* device-side action check (batch.py:92-106) */
+
+/* ---- modes (layout.py:60-62) ------------------------------------------ */
+#define TC_MODE_RESET 0
+#define TC_MODE_STEP 1
+
+/* ---- capacities (layout.py:64-66) ------------------------------------- */
+#define TC_MAX_ENTITIES 64
+#define TC_MAX_DOORS 32
+#define TC_MAX_OBS_W 1024
+#define TC_MAX_OBS_H 1024
+
+/*
+ * Read-only per-spec tables, field order = tables.py:257-261 (the order
+ * batch_kernel receives them in), plus the array extents that the Cython
+ * memoryviews carried implicitly. All pointers are HOST pointers when passed
+ * to tc_spec_create (which packs and uploads them once per spec, like
+ * build_tables, tables.py:92-184) and to the tc_host_* parity helpers.
+ */
+typedef struct tc_tables {
+  /* map group */
+  const uint8_t *kind;      /* u8  [h, w]   cell tags (C_FLOOR/C_WALL/C_DOOR)  */
+  const uint8_t *wcol;      /* u8  [h, w]   wall palette index                  */
+  const int16_t *didx;      /* i16 [h, w]   door index or -1                    */
+  const int16_t *eat;       /* i16 [h, w]   entity index or -1                  */
+  const uint8_t *dcol;      /* u8  [D]      door key colour                     */
+  const uint8_t *dlock;     /* u8  [D]      door locked flag                    */
+  const uint8_t *ekind;     /* u8  [E]      entity kind                         */
+  const uint8_t *ecol;      /* u8  [E]      entity colour (keys)                */
+  const double *epx;        /* f64 [E]      entity x (tile centre)              */
+  const double *epy;        /* f64 [E]                                          */
+  const double *spx;        /* f64 [S]      spawn x                             */
+  const double *spy;        /* f64 [S]                                          */
+  const int32_t *goal_ent;  /* i32 [G]      goal candidate entity indices       */
+  const double *dirs;       /* f64 [4, 2]   E, S, W, N headings                 */
+  /* render group */
+  const uint8_t *pal;       /* u8  [P, 3]   wall palette                        */
+  const uint8_t *door_rgb;  /* u8  [3, 3]                                       */
+  const uint8_t *key_rgb;   /* u8  [3, 3]                                       */
+  const uint8_t *goal_rgb;  /* u8  [3]                                          */
+  const uint8_t *med_box;   /* u8  [3]                                          */
+  const uint8_t *med_cross; /* u8  [3]                                          */
+  const uint8_t *ceil_rgb;  /* u8  [3]                                          */
+  const uint8_t *floor_rgb; /* u8  [3]                                          */
+  const double *coef;       /* f64 [obs_w]  camera-plane coefficient per column */
+  /* constants */
+  const double *fc;         /* f64 [11]     layout.py:8-19                      */
+  const int64_t *ic;        /* i64 [3]      layout.py:22-25                     */
+  const uint8_t *legal;     /* u8  [7]      legal action tags (tables.py:165)   */
+  /* extents */
+  int32_t h, w;             /* map tiles                                        */
+  int32_t n_doors, n_entities, n_spawns, n_goals, n_pal;
+  int32_t obs_h, obs_w;
+} tc_tables;
+
+/* Mutable per-env state, env index first (StateBlock, tables.py:187-215). */
+typedef struct tc_state {
+  double *px, *py, *dx, *dy, *health; /* f64 [N]    */
+  uint8_t *inv;                       /* u8  [N]    */
+  int64_t *t;                         /* i64 [N]    */
+  uint64_t *rkey, *rctr;              /* u64 [N]    */
+  uint8_t *done;                      /* u8  [N]    */
+  int32_t *agoal;                     /* i32 [N]    */
+  uint8_t *dopen;                     /* u8  [N, D] */
+  uint8_t *ealive;                    /* u8  [N, E] */
+} tc_state;
+
+/* Per-call outputs (OutBlock, tables.py:223-245) plus optional debug taps. */
+typedef struct tc_out {
+  uint8_t *frames;    /* u8  [N, obs_h, obs_w, 3] (required)                    */
+  double *zbuf;       /* f64 [N, obs_w]   optional (NULL = not written)          */
+  double *rewards;    /* f64 [N]          required in MODE_STEP                  */
+  uint8_t *dones;     /* u8  [N]          required in MODE_STEP                  */
+  uint8_t *truncs;    /* u8  [N]          required in MODE_STEP                  */
+  uint32_t *events;   /* u32 [N]          required in MODE_STEP                  */
+  int32_t *statuses;  /* i32 [N]          required                               */
+  /* debug taps for the north-star per-item parity checks (NULL = off):        */
+  int32_t *rayinfo;   /* i32 [N, obs_w, 4] (mapx, mapy, side, steps) per column  */
+  uint64_t *spritevis;/* u64 [N]   bit e set = entity e drew >= 1 pixel column   */
+} tc_out;
+
+/* Device-side counters written by the step kernel (read lazily by the host;
+ * no per-step synchronisation). */
+typedef struct tc_counters {
+  uint64_t violations;   /* collision-invariant violations (batch.py:133)   */
+  uint32_t bad_status;   /* OR of all non-OK statuses this call             */
+  uint32_t pad;
+} tc_counters;
+
+typedef struct tc_spec tc_spec; /* opaque, device-resident packed tables */
+
+/* ABI / build info. */
+int tc_abi_version(void);
+const char *tc_last_error(void);
+const char *tc_build_info(void);
+
+/* Pack + upload a spec's tables once (replaces build_tables' device half,
+ * tables.py:92-184). `host` points at host arrays. */
+int tc_spec_create(const tc_tables *host, tc_spec **out);
+int tc_spec_destroy(tc_spec *spec);
+
+/* Reset (mode 0) or step (mode 1) envs [0, n) in place
+ * (replaces backend.batch_kernel, _core.pyx:715-763 / _pycore.py:346-387).
+ * `state`/`out` hold DEVICE pointers; `actions_dev` is i64[n] (ignored in
+ * reset mode). `counters_dev` (device, may be NULL) accumulates violations
+ * and status bits; the reference returns the violation count synchronously
+ * instead (tc_host_batch_kernel below does). Asynchronous on `stream`. */
+int tc_batch_kernel(const tc_spec *spec, const tc_state *state,
+                    const int64_t *actions_dev, const tc_out *out, int64_t n,
+                    int32_t mode, int32_t auto_reset, int32_t validate,
+                    tc_counters *counters_dev, void *stream);
+
+/* K fused steps in one launch with on-device uniform-random actions drawn
+ * exactly as batch.policy_actions (batch.py:141-153) would draw them for
+ * steps [step0, step0+K) of an (n_total)-env rollout whose env 0 is global
+ * env `base`. Frames of step k go to out->frames + (k % frame_ring) * N*H*W*3
+ * (a ring of frame_ring >= 1 frame blocks, or K for a full rollout buffer).
+ * rewards/dones/truncs/events (if non-NULL) are [K, N]. Auto-reset is on. */
+int tc_rollout(const tc_spec *spec, const tc_state *state, const tc_out *out,
+               int64_t n, int64_t base, int64_t n_total, uint64_t policy_key,
+               int64_t step0, int32_t k_steps, int32_t frame_ring,
+               tc_counters *counters_dev, void *stream);
+
+/* Per-env RNG streams: rkey[i] = split(from_seed(seed), base+i).key,
+ * rctr[i] = 0 (replaces the host loop batch.py:81-85; rng.py:96-99). */
+int tc_seed_streams(uint64_t seed, int64_t base, int64_t n, uint64_t *rkey_dev,
+                    uint64_t *rctr_dev, void *stream);
+
+/* Uniform-random actions for one step of a seeded rollout
+ * (batch.py:141-153, rng.py:102-129): actions[i] = action_tags[
+ * mulhi(mix(key + (step*n_total + base + i)*GOLDEN), n_tags)]. */
+int tc_policy_actions(uint64_t policy_key, int64_t step, int64_t n_total,
+                      int64_t base, int64_t n, const int64_t *action_tags_host,
+                      int32_t n_tags, int64_t *actions_dev, void *stream);
+
+/* Host-pointer parity entry points (replace the module-level cast_ray /
+ * render_into / batch_kernel, _core.pyx:683-763). They copy H2D, run the
+ * SAME device code as the batch path, copy D2H and synchronise. */
+int tc_host_cast_ray(const uint8_t *kind, const int16_t *didx,
+                     const uint8_t *dopen, int32_t h, int32_t w, double ox,
+                     double oy, double rx, double ry, int32_t *status,
+                     int32_t *mapx, int32_t *mapy, int32_t *side, double *perp,
+                     double *wall_u, int32_t *steps);
+int tc_host_render_into(const tc_tables *host, double px, double py, double dx,
+                        double dy, const uint8_t *dopen_row,
+                        const uint8_t *ealive_row, int32_t agoal,
+                        uint8_t *frame, double *zbuf, int32_t *status);
+int tc_host_batch_kernel(const tc_tables *host, const tc_state *state_host,
+                         const int64_t *actions_host, const tc_out *out_host,
+                         int64_t n, int32_t mode, int32_t auto_reset,
+                         int32_t validate, int64_t *violations);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILECAST_B200_H */

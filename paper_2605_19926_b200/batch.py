@@ -1,0 +1,285 @@
+"""Batched reset/step over N same-spec environments, device resident.
+
+API of the reference's ``tilecast.batch`` (/root/reference/pkg/src/tilecast/batch.py:27-179):
+``batch_reset``, ``batch_step`` (auto-reset, ``reuse`` double-buffering,
+``validate``), ``policy_actions``, ``throughput_probe``. Differences, all
+consequences of keeping the step on the GPU with no host round trip:
+
+* observations, state and per-step outputs are torch CUDA tensors
+  (``BatchState.frames`` is ``uint8[N, H, W, 3]`` in HBM);
+* ``batch_step`` returns device tensors ``(rewards f64[N], dones bool[N])``;
+* per-env engine faults (unsealed maps, illegal actions passed as a device
+  tensor) are accumulated in device counters and raised by
+  ``BatchState.check()`` -- called by ``state()``/``states`` and, with
+  ``validate=True`` or ``sync_checks=True``, by ``batch_step`` itself (the
+  reference raises inside every call, tables.py:267-272, batch.py:133-135);
+* the per-env RNG split (a host loop in the reference, batch.py:81-85) and
+  the policy draw run on the device; they are bit-identical.
+
+Envs can be a shard of a larger batch: ``base`` / ``n_total`` make env i use
+the global index ``base + i`` for its reset stream and policy counters, so a
+trajectory does not depend on how many GPUs the batch is split over.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import layout as L
+from . import rng
+from .dynamics import ACTION_NAMES, Action, EnvState, state_from_arrays
+from .engine import (DeviceOut, DeviceSpec, DeviceState, device_spec, launch_batch,
+                     new_counters, read_counters, resolve_device, stream_ptr)
+from .geometry import ContractError
+from .suite import EnvSpec
+
+
+@dataclass
+class BatchState:
+    """N environments' device state plus their observation block.
+
+    With ``reuse=True`` stepping recycles the predecessor's buffers: a state
+    is then valid only until its successor is stepped (batch.py:31-34).
+    """
+
+    spec: EnvSpec
+    n: int
+    _ds: DeviceSpec
+    _sb: DeviceState
+    _ob: DeviceOut
+    _counters: torch.Tensor
+    base: int = 0
+    n_total: int = 0
+    _retired: tuple = field(default=(), repr=False)
+    _stage: "_ActionStage | None" = field(default=None, repr=False)
+
+    @property
+    def device(self) -> torch.device:
+        return self._ds.device
+
+    @property
+    def frames(self) -> torch.Tensor:
+        """(n, obs_height, obs_width, 3) uint8 observations in HBM."""
+        return self._ob.frames
+
+    def check(self) -> None:
+        """Raise for faults accumulated on the device since the batch began."""
+        viol, bad = read_counters(self._counters)
+        if bad & (1 << L.ST_BAD_ACTION):
+            raise ContractError(
+                f"an action outside {self.spec.id!r}'s action set reached the device")
+        if bad & ((1 << L.ST_ESCAPED) | (1 << L.ST_STEP_BUDGET)):
+            raise RuntimeError("render invariant violated: " + (
+                "ray escaped the map (unsealed?)" if bad & (1 << L.ST_ESCAPED)
+                else "ray exceeded its boundary-step budget"))
+        if viol:
+            raise RuntimeError(f"collision invariant violated in {viol} environment step(s)")
+
+    def host_state(self) -> dict:
+        return self._sb.to_host()
+
+    def state(self, i: int) -> EnvState:
+        if not (0 <= i < self.n):
+            raise ContractError(f"environment index {i} out of range [0, {self.n})")
+        self.check()
+        return state_from_arrays(self._sb.to_host(), i)
+
+    @property
+    def states(self) -> tuple[EnvState, ...]:
+        self.check()
+        a = self._sb.to_host()
+        return tuple(state_from_arrays(a, i) for i in range(self.n))
+
+    @property
+    def last_terminated(self) -> torch.Tensor:
+        return (self._ob.dones != 0) & (self._ob.truncs == 0)
+
+    @property
+    def last_truncated(self) -> torch.Tensor:
+        return self._ob.truncs != 0
+
+    @property
+    def last_events(self) -> np.ndarray:
+        return self._ob.events.cpu().numpy().view(np.uint32)
+
+
+class _ActionStage:
+    """Two pinned host buffers + device buffers for async action upload.
+
+    A buffer is rewritten only after the event recorded behind its previous
+    H2D copy has fired, so no copy ever reads a half-written buffer."""
+
+    def __init__(self, n: int, device: torch.device):
+        self.pinned = [torch.empty(n, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self.dev = [torch.empty(n, dtype=torch.int64, device=device) for _ in range(2)]
+        self.events = [torch.cuda.Event() for _ in range(2)]
+        self.k = 0
+
+    def put(self, acts: np.ndarray) -> torch.Tensor:
+        self.k ^= 1
+        k = self.k
+        self.events[k].synchronize()
+        self.pinned[k].numpy()[:] = acts
+        self.dev[k].copy_(self.pinned[k], non_blocking=True)
+        self.events[k].record(torch.cuda.current_stream(self.dev[k].device))
+        return self.dev[k]
+
+
+def batch_reset(spec: EnvSpec, n: int, seed: int, *, device=None, base: int = 0,
+                n_total: int | None = None, debug: bool = False) -> BatchState:
+    """Reset n envs; env i draws from stream split(from_seed(seed), base + i)."""
+    if n < 1:
+        raise ContractError(f"batch size must be >= 1, got {n}")
+    dev = resolve_device(device)
+    ds = device_spec(spec, dev)
+    t = spec.tables
+    sb = DeviceState.alloc(n, t.n_doors, t.n_entities, dev)
+    ob = DeviceOut.alloc(n, t.obs_height, t.obs_width, dev, debug=debug)
+    counters = new_counters(dev)
+    with torch.cuda.device(dev):
+        N.check(N.lib().tc_seed_streams(seed & rng.M64, base, n, N.ptr(sb.rkey),
+                                        N.ptr(sb.rctr), stream_ptr(dev)), "tc_seed_streams")
+    launch_batch(ds, sb, None, ob, n, L.MODE_RESET, False, False, counters)
+    return BatchState(spec=spec, n=n, _ds=ds, _sb=sb, _ob=ob, _counters=counters,
+                      base=base, n_total=n_total if n_total is not None else base + n)
+
+
+def _coerce_actions(bs: BatchState, actions) -> torch.Tensor:
+    """Host-side contract checks (batch.py:92-106), then an async H2D copy
+    through a pinned staging buffer. CUDA tensors are checked on the device."""
+    if isinstance(actions, torch.Tensor) and actions.is_cuda:
+        if actions.shape != (bs.n,):
+            raise ContractError(f"actions must have shape ({bs.n},), got {tuple(actions.shape)}")
+        return actions.to(torch.int64).contiguous()
+    acts = np.asarray(actions.cpu() if isinstance(actions, torch.Tensor) else actions,
+                      dtype=np.int64)
+    if acts.shape != (bs.n,):
+        raise ContractError(f"actions must have shape ({bs.n},), got {acts.shape}")
+    if acts.min(initial=0) < 0 or acts.max(initial=0) >= L.A_COUNT:
+        raise ContractError(f"action tags must be in [0, {L.A_COUNT})")
+    legal = bs.spec.tables.legal
+    ok = legal[acts] != 0
+    if not ok.all():
+        bad = int(acts[~ok][0])
+        names = ", ".join(ACTION_NAMES[a] for a in bs.spec.action_set)
+        raise ContractError(f"action {ACTION_NAMES[Action(bad)]!r} is not in "
+                            f"{bs.spec.id!r}'s action set ({names})")
+    if bs._stage is None:
+        bs._stage = _ActionStage(bs.n, bs.device)
+    return bs._stage.put(acts)
+
+
+def batch_step(bs: BatchState, actions: Sequence[Action | int] | np.ndarray | torch.Tensor, *,
+               validate: bool = False, reuse: bool = False,
+               sync_checks: bool = False) -> tuple[BatchState, torch.Tensor, torch.Tensor]:
+    """Step every env once; finished episodes auto-reset in the same launch
+    (their frame shows the new episode; the terminal reward / done flag are
+    still reported). Returns (next_state, rewards, dones) as device tensors."""
+    spec, t = bs.spec, bs.spec.tables
+    acts = _coerce_actions(bs, actions)
+    if reuse and bs._retired:
+        sb, ob = bs._retired
+    else:
+        sb = DeviceState.alloc(bs.n, t.n_doors, t.n_entities, bs.device)
+        ob = DeviceOut.alloc(bs.n, t.obs_height, t.obs_width, bs.device,
+                             debug=bs._ob.zbuf is not None)
+    sb.copy_from(bs._sb)
+    launch_batch(bs._ds, sb, acts, ob, bs.n, L.MODE_STEP, True, validate, bs._counters)
+    new = BatchState(spec=spec, n=bs.n, _ds=bs._ds, _sb=sb, _ob=ob, _counters=bs._counters,
+                     base=bs.base, n_total=bs.n_total,
+                     _retired=(bs._sb, bs._ob) if reuse else (),
+                     _stage=bs._stage)
+    if validate or sync_checks:
+        new.check()
+    return new, ob.rewards, ob.dones != 0
+
+
+def batch_step_inplace(bs: BatchState, actions: torch.Tensor) -> BatchState:
+    """Throughput form of batch_step: mutate bs's state in place (no state
+    copy), one kernel launch, no host work beyond the launch."""
+    launch_batch(bs._ds, bs._sb, actions, bs._ob, bs.n, L.MODE_STEP, True, False,
+                 bs._counters)
+    return bs
+
+
+def policy_actions(spec: EnvSpec, n: int, steps: int, seed: int = 0) -> np.ndarray:
+    """The (steps, n) uniform-random action table of a seeded rollout
+    (batch.py:141-153), computed on the host like the reference."""
+    tags = np.array([int(a) for a in spec.action_set], dtype=np.int64)
+    counters = np.arange(steps * n, dtype=np.uint64).reshape(steps, n)
+    return tags[rng.policy_uniform(rng.policy_key(seed), counters, tags.shape[0])]
+
+
+def policy_actions_device(spec: EnvSpec, step: int, n: int, seed: int, *, base: int = 0,
+                          n_total: int | None = None, out: torch.Tensor | None = None,
+                          device=None) -> torch.Tensor:
+    """Row ``step`` of policy_actions(spec, n_total, ..., seed) for envs
+    [base, base+n), drawn on the device."""
+    dev = resolve_device(device if out is None else out.device)
+    if out is None:
+        out = torch.empty(n, dtype=torch.int64, device=dev)
+    tags = np.array([int(a) for a in spec.action_set], dtype=np.int64)
+    with torch.cuda.device(dev):
+        N.check(N.lib().tc_policy_actions(
+            rng.policy_key(seed), step, n_total if n_total is not None else base + n, base, n,
+            tags.ctypes.data, tags.shape[0], N.ptr(out), stream_ptr(dev)), "tc_policy_actions")
+    return out
+
+
+def rollout(bs: BatchState, k_steps: int, seed: int, *, step0: int = 0,
+            frames: torch.Tensor | None = None, record: bool = False) -> dict:
+    """K fused steps in ONE launch with the seeded uniform policy drawn on the
+    device (== batch_step with policy_actions(spec, n_total, ..., seed)
+    rows step0..step0+K-1). ``frames`` is a [R, N, H, W, 3] ring (R >= 1;
+    default: the batch's own frame block, R = 1); with ``record`` the
+    per-step rewards/dones/truncs/events come back as [K, N] tensors."""
+    t = bs.spec.tables
+    dev = bs.device
+    ring = bs._ob.frames.unsqueeze(0) if frames is None else frames
+    if ring.dim() != 5 or tuple(ring.shape[1:]) != (bs.n, t.obs_height, t.obs_width, 3):
+        raise ContractError("frames must be [R, N, H, W, 3] uint8")
+    res = {}
+    if record:
+        res = dict(
+            rewards=torch.zeros((k_steps, bs.n), dtype=torch.float64, device=dev),
+            dones=torch.zeros((k_steps, bs.n), dtype=torch.uint8, device=dev),
+            truncs=torch.zeros((k_steps, bs.n), dtype=torch.uint8, device=dev),
+            events=torch.zeros((k_steps, bs.n), dtype=torch.int32, device=dev))
+    o = N.TcOut()
+    o.frames = N.ptr(ring)
+    o.statuses = N.ptr(bs._ob.statuses)
+    for k, v in res.items():
+        setattr(o, k, N.ptr(v))
+    with torch.cuda.device(dev):
+        N.check(N.lib().tc_rollout(
+            bs._ds.handle, N.C.byref(bs._sb.c_struct()), N.C.byref(o), bs.n, bs.base,
+            bs.n_total, rng.policy_key(seed), step0, k_steps, ring.shape[0],
+            N.ptr(bs._counters), stream_ptr(dev)), "tc_rollout")
+    res["frames"] = ring
+    return res
+
+
+def throughput_probe(spec: EnvSpec, n: int, steps: int, seed: int = 0, *,
+                     device=None) -> float:
+    """Aggregate env-steps/s under the seeded uniform policy, wall-clock,
+    through batch_step with host actions (batch.py:156-179 semantics)."""
+    if n < 1 or steps < 1:
+        raise ContractError("n and steps must both be >= 1")
+    bs = batch_reset(spec, n, seed, device=device)
+    all_actions = policy_actions(spec, n, steps, seed)
+    for s in range(min(3, steps)):
+        bs, _, _ = batch_step(bs, all_actions[s], reuse=True)
+    torch.cuda.synchronize(bs.device)
+    start = time.perf_counter()
+    for s in range(steps):
+        bs, _, _ = batch_step(bs, all_actions[s], reuse=True)
+    torch.cuda.synchronize(bs.device)
+    elapsed = time.perf_counter() - start
+    bs.check()
+    return (n * steps) / elapsed

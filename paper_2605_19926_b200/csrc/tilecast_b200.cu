@@ -1,0 +1,1514 @@
+// tilecast_b200.cu -- B200-native (sm_100a) fused batched environment step.
+//
+// One launch steps N independent environments: dynamics (turn / slide move /
+// doors / pickups / health / termination), auto-reset with the counter-based
+// RNG, DDA ray cast per screen column, z-buffered sprite billboards, and the
+// uint8 RGB frame written row-major to HBM with TMA bulk stores.
+//
+// Semantics: bit-exact with the reference's kernels
+// (/root/reference/pkg/src/tilecast/backend/_pycore.py, transcribed in
+// _core.pyx); every floating-point expression keeps the reference's operation
+// order and is compiled with --fmad=false (no contraction), IEEE division and
+// sqrt. Citations below are _pycore.py:line unless stated.
+//
+// Work decomposition:
+//   * one warp owns one environment at a time; CTAs loop over envs
+//     (grid sized to the SM count x occupancy, so every launch is one wave);
+//   * dynamics run warp-uniform (every lane computes the same scalars);
+//   * lane L casts the rays of columns L, L+32, ... (its z-buffer entries stay
+//     in registers for the sprite pass);
+//   * the frame is produced in horizontal bands staged in shared memory:
+//     lanes compose 4-pixel (12-byte) groups with PRMT byte packing, sprites
+//     overwrite their pixels column-by-column in draw order, and one lane
+//     ships the band with cp.async.bulk (TMA bulk copy) while the warp
+//     composes the next band into the other buffer.
+//   * the packed tile map is staged once per CTA into shared memory.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tilecast_b200.h"
+
+namespace {
+
+// ---------------------------------------------------------------- constants
+// layout.py:8-66 (mirrored in paper_2605_19926_b200/layout.py)
+enum { FC_MOVE_SPEED = 0, FC_RADIUS, FC_TURN_COS, FC_TURN_SIN, FC_ATTEN,
+       FC_GOAL_REWARD, FC_LIVING_REWARD, FC_HEALTH_DECAY, FC_HEALTH_RESTORE,
+       FC_SPRITE_K, FC_MIN_SPRITE_DEPTH, FC_COUNT };
+enum { A_FORWARD = 0, A_BACKWARD, A_TURN_LEFT, A_TURN_RIGHT, A_STRAFE_LEFT,
+       A_STRAFE_RIGHT, A_NOOP, A_COUNT };
+enum { C_FLOOR = 0, C_WALL = 1, C_DOOR = 2 };
+enum { K_KEY = 0, K_GOAL = 1, K_MEDKIT = 2 };
+enum { EV_KEY_BASE_BIT = 0, EV_DOOR_BASE_BIT = 3, EV_MEDKIT_BIT = 6,
+       EV_GOAL_BIT = 7, EV_DIED_BIT = 8, EV_TRUNCATED_BIT = 9 };
+enum { MODE_RESET = 0, MODE_STEP = 1, MODE_RENDER = 2 };
+
+constexpr double PLANE_HALF_WIDTH = 0.66;  // geometry.py:18
+constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ULL;
+constexpr uint64_t MIX2 = 0x94D049BB133111EBULL;
+constexpr uint64_t SPLIT_SALT = 0x3C6EF372FE94F82AULL;
+
+constexpr int WARPS_PER_CTA = 4;
+constexpr int BAND_BYTES_TARGET = 3072;       // per staging buffer
+constexpr int SMEM_MAP_MAX_CELLS = 8192;      // stage map in smem up to this
+
+// packed cell word: bits 0-7 = wall colour or door index, 8-9 = cell tag,
+// 16-23 = entity index + 1 (0 = no entity on the tile)
+constexpr uint32_t CELL_TAG_SHIFT = 8;
+constexpr uint32_t CELL_EAT_SHIFT = 16;
+
+// ------------------------------------------------------------- device spec
+struct SpecDev {
+  const uint32_t* cell;     // [h*w] packed cells
+  const uint32_t* pal;      // [n_pal] wall colours, r | g<<8 | b<<16
+  const uint32_t* doorrgb;  // [D] door_rgb[dcol[d]]
+  const uint8_t* dcol;      // [D]
+  const uint8_t* dlock;     // [D]
+  const double* epx;        // [E]
+  const double* epy;        // [E]
+  const uint8_t* ekind;     // [E]
+  const uint8_t* ecol;      // [E]
+  const double* spx;        // [S]
+  const double* spy;        // [S]
+  const int32_t* goal_ent;  // [G]
+  const double* coef;       // [obs_w]
+  double fc[FC_COUNT];
+  double dirs[8];
+  long long max_steps;
+  int goal_mode, use_health;
+  uint32_t ceil_rgb, floor_rgb, goal_rgb, med_box, med_cross, key_rgb[3];
+  uint32_t legal_mask;
+  int h, w, n_doors, n_ent, n_spawns, n_goals, n_pal, obs_h, obs_w;
+  // launch geometry derived on the host
+  int band_rows;     // rows per staging band
+  int band_stride;   // bytes per staging buffer (16-aligned)
+  int smem_map;      // 1 = stage cells into shared memory
+  int quads;         // 1 = obs_w % 4 == 0 (4-pixel packed compose)
+  int bulk;          // 1 = frame rows are 16-byte multiples (TMA bulk store)
+  int warp_smem;     // bytes of per-warp shared memory
+};
+
+struct StateDev {
+  double *px, *py, *dx, *dy, *health;
+  uint8_t* inv;
+  long long* t;
+  unsigned long long *rkey, *rctr;
+  uint8_t* done;
+  int32_t* agoal;
+  uint8_t* dopen;
+  uint8_t* ealive;
+};
+
+struct OutDev {
+  uint8_t* frames;
+  double* zbuf;
+  double* rewards;
+  uint8_t* dones;
+  uint8_t* truncs;
+  uint32_t* events;
+  int32_t* statuses;
+  int32_t* rayinfo;
+  unsigned long long* spritevis;
+};
+
+struct RolloutArgs {
+  unsigned long long policy_key;
+  long long base, n_total, step0;
+  int k_steps, frame_ring;
+  int n_tags;
+  int tags[A_COUNT];
+};
+
+// per-env register state, warp-uniform
+struct Env {
+  double x, y, dx, dy, health;
+  long long t;
+  unsigned long long rkey, rctr;
+  uint32_t dmask;       // bit d = door d open
+  unsigned long long emask;  // bit e = entity e alive
+  int agoal;
+  uint32_t inv;
+  int done;
+};
+
+// sprite record in draw order (far -> near), _pycore.py:219-252
+struct SpriteRec {
+  double dep, ks, halfk;
+  int vtop, denom, r0, r1;
+  uint32_t s1, s2;  // shaded main / secondary colour
+  int kd, ent;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= MIX1;
+  x ^= x >> 27;
+  x *= MIX2;
+  x ^= x >> 31;
+  return x;
+}
+
+// _pycore.py:27-35
+__device__ __forceinline__ uint64_t draw_below(uint64_t key, unsigned long long& ctr,
+                                               uint64_t n) {
+  const uint64_t x = mix64(key + ctr * GOLDEN);
+  ctr += 1;
+  return __umul64hi(x, n);
+}
+
+__device__ __forceinline__ uint32_t rgb_scale(uint32_t rgb, double shade) {
+  // (int)(channel * shade) per channel, _pycore.py:168-170
+  const int r = (int)((double)(rgb & 0xff) * shade);
+  const int g = (int)((double)((rgb >> 8) & 0xff) * shade);
+  const int b = (int)((double)((rgb >> 16) & 0xff) * shade);
+  return (uint32_t)(r & 0xff) | ((uint32_t)(g & 0xff) << 8) | ((uint32_t)(b & 0xff) << 16);
+}
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+// DDA, _pycore.py:38-96. `cell` may point at shared or global memory.
+struct RayHit {
+  int status, mapx, mapy, side, steps;
+  double perp, wu;
+};
+
+__device__ __forceinline__ RayHit cast_ray(const uint32_t* __restrict__ cell, int h, int w,
+                                           uint32_t dmask, double ox, double oy,
+                                           double rx, double ry) {
+  int mapx = (int)floor(ox);
+  int mapy = (int)floor(oy);
+  double ddx, ddy, sdx, sdy;
+  int stepx, stepy;
+  if (rx != 0.0) {
+    ddx = fabs(1.0 / rx);
+    stepx = rx > 0.0 ? 1 : -1;
+    sdx = rx > 0.0 ? (((double)mapx + 1.0) - ox) * ddx : (ox - (double)mapx) * ddx;
+  } else {
+    ddx = dinf();
+    stepx = 0;
+    sdx = dinf();
+  }
+  if (ry != 0.0) {
+    ddy = fabs(1.0 / ry);
+    stepy = ry > 0.0 ? 1 : -1;
+    sdy = ry > 0.0 ? (((double)mapy + 1.0) - oy) * ddy : (oy - (double)mapy) * ddy;
+  } else {
+    ddy = dinf();
+    stepy = 0;
+    sdy = dinf();
+  }
+  const int limit = 2 * (w + h);
+  int side = 0, steps = 0;
+  RayHit r;
+  for (;;) {
+    if (sdx < sdy) {  // ties step Y (_pycore.py:70)
+      sdx += ddx;
+      mapx += stepx;
+      side = 0;
+    } else {
+      sdy += ddy;
+      mapy += stepy;
+      side = 1;
+    }
+    steps += 1;
+    if (steps > limit || (unsigned)mapx >= (unsigned)w || (unsigned)mapy >= (unsigned)h) {
+      r.status = steps > limit ? TC_ST_STEP_BUDGET : TC_ST_ESCAPED;
+      r.mapx = mapx; r.mapy = mapy; r.side = side; r.steps = steps;
+      r.perp = 0.0; r.wu = 0.0;
+      return r;
+    }
+    const uint32_t cw = cell[mapy * w + mapx];
+    const uint32_t tag = (cw >> CELL_TAG_SHIFT) & 3u;
+    if (tag == C_WALL) break;
+    if (tag == C_DOOR && ((dmask >> (cw & 31u)) & 1u) == 0) break;
+  }
+  double perp, wu;
+  if (side == 0) {
+    perp = sdx - ddx;
+    wu = oy + perp * ry;
+  } else {
+    perp = sdy - ddy;
+    wu = ox + perp * rx;
+  }
+  wu -= floor(wu);
+  r.status = TC_ST_OK;
+  r.mapx = mapx; r.mapy = mapy; r.side = side; r.steps = steps;
+  r.perp = perp; r.wu = wu;
+  return r;
+}
+
+// _pycore.py:99-129, split so per-column (aa, ea) and per-row (v, ev) terms
+// are computed once and reused: identical doubles, identical comparisons.
+__device__ __forceinline__ int sprite_mask(int kd, double aa, double ea, double v, double ev) {
+  if (kd == K_GOAL) {
+    double dv = v - 0.5;
+    if (dv < 0.0) dv = -dv;
+    return (aa + dv * 2.0 <= 0.8) ? 1 : 0;
+  }
+  if (kd == K_KEY) {
+    const double e = ea * ea + ev * ev;
+    if (0.30 <= e && e <= 1.0) return 1;
+    if (aa <= 0.07 && 0.30 <= v && v <= 0.85) return 1;
+    if (aa <= 0.24 && 0.62 <= v && v <= 0.70) return 1;
+    if (aa <= 0.24 && 0.76 <= v && v <= 0.84) return 1;
+    return 0;
+  }
+  if (aa <= 0.10 && 0.32 <= v && v <= 0.73) return 1;
+  if (aa <= 0.38 && 0.47 <= v && v <= 0.60) return 1;
+  if (aa <= 0.60 && 0.25 <= v && v <= 0.80) return 2;
+  return 0;
+}
+
+// _pycore.py:274-304 (disc vs grid, strict <)
+__device__ __forceinline__ bool blocked(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                        uint32_t dmask, double cx, double cy, double radius) {
+  const int tx0 = (int)floor(cx - radius), tx1 = (int)floor(cx + radius);
+  const int ty0 = (int)floor(cy - radius), ty1 = (int)floor(cy + radius);
+  const double r2 = radius * radius;
+  for (int ty = ty0; ty <= ty1; ty++) {
+    for (int tx = tx0; tx <= tx1; tx++) {
+      if (tx < 0 || tx >= S.w || ty < 0 || ty >= S.h) return true;
+      const uint32_t cw = cell[ty * S.w + tx];
+      const uint32_t tag = (cw >> CELL_TAG_SHIFT) & 3u;
+      if (tag == C_FLOOR) continue;
+      if (tag == C_DOOR && ((dmask >> (cw & 31u)) & 1u) != 0) continue;
+      double nx = cx;
+      if (nx < tx) nx = tx;
+      else if (nx > tx + 1.0) nx = tx + 1.0;
+      double ny = cy;
+      if (ny < ty) ny = ty;
+      else if (ny > ty + 1.0) ny = ty + 1.0;
+      const double ddx = cx - nx, ddy = cy - ny;
+      if (ddx * ddx + ddy * ddy < r2) return true;
+    }
+  }
+  return false;
+}
+
+// _pycore.py:307-343
+__device__ __forceinline__ uint32_t touch_doors(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                                uint32_t& dmask, double cx, double cy,
+                                                double radius, uint32_t inv) {
+  uint32_t events = 0;
+  const int tx0 = (int)floor(cx - radius), tx1 = (int)floor(cx + radius);
+  const int ty0 = (int)floor(cy - radius), ty1 = (int)floor(cy + radius);
+  const double r2 = radius * radius;
+  for (int ty = ty0; ty <= ty1; ty++) {
+    for (int tx = tx0; tx <= tx1; tx++) {
+      if (tx < 0 || tx >= S.w || ty < 0 || ty >= S.h) continue;
+      const uint32_t cw = cell[ty * S.w + tx];
+      if (((cw >> CELL_TAG_SHIFT) & 3u) != C_DOOR) continue;
+      const int di = (int)(cw & 31u);
+      if ((dmask >> di) & 1u) continue;
+      double nx = cx;
+      if (nx < tx) nx = tx;
+      else if (nx > tx + 1.0) nx = tx + 1.0;
+      double ny = cy;
+      if (ny < ty) ny = ty;
+      else if (ny > ty + 1.0) ny = ty + 1.0;
+      const double ddx = cx - nx, ddy = cy - ny;
+      if (ddx * ddx + ddy * ddy >= r2) continue;
+      const int dc = S.dcol[di];
+      if (S.dlock[di] != 0 && ((inv >> dc) & 1u) == 0) continue;
+      dmask |= 1u << di;
+      events |= 1u << (EV_DOOR_BASE_BIT + dc);
+    }
+  }
+  return events;
+}
+
+// _pycore.py:390-414: draws in the contract order spawn, heading, goal
+__device__ __forceinline__ void reset_draws(const SpecDev& S, Env& e) {
+  unsigned long long ctr = e.rctr;
+  uint64_t v = draw_below(e.rkey, ctr, (uint64_t)S.n_spawns);
+  e.x = S.spx[v];
+  e.y = S.spy[v];
+  v = draw_below(e.rkey, ctr, 4);
+  e.dx = S.dirs[2 * v];
+  e.dy = S.dirs[2 * v + 1];
+  if (S.goal_mode == 1 && S.n_goals > 0) {
+    v = draw_below(e.rkey, ctr, (uint64_t)S.n_goals);
+    e.agoal = S.goal_ent[v];
+  } else if (S.n_goals > 0) {
+    e.agoal = S.goal_ent[0];
+  } else {
+    e.agoal = -1;
+  }
+  e.rctr = ctr;
+  e.health = 100.0;
+  e.inv = 0;
+  e.t = 0;
+  e.done = 0;
+  e.dmask = 0;
+  e.emask = S.n_ent >= 64 ? ~0ULL : ((1ULL << S.n_ent) - 1ULL);
+}
+
+struct StepOut {
+  double reward;
+  uint32_t events;
+  int done, trunc, violation;
+};
+
+// _pycore.py:431-531 (everything before the render / auto-reset branch)
+__device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                                 Env& e, int act, int validate) {
+  StepOut o;
+  o.events = 0;
+  o.reward = 0.0;
+  o.violation = 0;
+  int terminated = 0, truncated = 0;
+  double x = e.x, y = e.y, dxx = e.dx, dyy = e.dy;
+  const double ms = S.fc[FC_MOVE_SPEED], radius = S.fc[FC_RADIUS];
+  if (act == A_TURN_LEFT || act == A_TURN_RIGHT) {
+    const double s = act == A_TURN_RIGHT ? S.fc[FC_TURN_SIN] : -S.fc[FC_TURN_SIN];
+    const double cs = S.fc[FC_TURN_COS];
+    const double ndx = dxx * cs - dyy * s;
+    const double ndy = dxx * s + dyy * cs;
+    const double nrm = sqrt(ndx * ndx + ndy * ndy);
+    dxx = ndx / nrm;
+    dyy = ndy / nrm;
+  } else if (act != A_NOOP) {
+    double mvx = 0.0, mvy = 0.0;
+    if (act == A_FORWARD) { mvx = ms * dxx; mvy = ms * dyy; }
+    else if (act == A_BACKWARD) { mvx = -ms * dxx; mvy = -ms * dyy; }
+    else if (act == A_STRAFE_LEFT) { mvx = ms * dyy; mvy = -ms * dxx; }
+    else if (act == A_STRAFE_RIGHT) { mvx = -ms * dyy; mvy = ms * dxx; }
+    const double nx = x + mvx;
+    o.events |= touch_doors(S, cell, e.dmask, nx, y, radius, e.inv);
+    if (!blocked(S, cell, e.dmask, nx, y, radius)) x = nx;
+    const double ny = y + mvy;
+    o.events |= touch_doors(S, cell, e.dmask, x, ny, radius, e.inv);
+    if (!blocked(S, cell, e.dmask, x, ny, radius)) y = ny;
+    if (validate && blocked(S, cell, e.dmask, x, y, radius)) o.violation = 1;
+  }
+  // pickups on the agent-centre tile only, _pycore.py:490-507
+  const int ctx = (int)floor(x), cty = (int)floor(y);
+  const int ent = (int)((cell[cty * S.w + ctx] >> CELL_EAT_SHIFT) & 0xffu) - 1;
+  if (ent >= 0 && ((e.emask >> ent) & 1ULL)) {
+    const int kd = S.ekind[ent];
+    if (kd == K_KEY) {
+      const int col = S.ecol[ent];
+      e.inv = (e.inv | (1u << col)) & 0xffu;
+      e.emask &= ~(1ULL << ent);
+      o.events |= 1u << (EV_KEY_BASE_BIT + col);
+    } else if (kd == K_MEDKIT) {
+      e.emask &= ~(1ULL << ent);
+      const double hv = e.health + S.fc[FC_HEALTH_RESTORE];
+      e.health = hv > 100.0 ? 100.0 : hv;
+      o.events |= 1u << EV_MEDKIT_BIT;
+    } else if (kd == K_GOAL && ent == e.agoal) {
+      o.reward = o.reward + S.fc[FC_GOAL_REWARD];
+      terminated = 1;
+      o.events |= 1u << EV_GOAL_BIT;
+    }
+  }
+  // health layer, _pycore.py:509-516
+  if (S.use_health != 0 && terminated == 0) {
+    o.reward = o.reward + S.fc[FC_LIVING_REWARD];
+    e.health = e.health - S.fc[FC_HEALTH_DECAY];
+    if (e.health <= 0.0) {
+      e.health = 0.0;
+      terminated = 1;
+      o.reward = 0.0;
+      o.events |= 1u << EV_DIED_BIT;
+    }
+  }
+  e.t = e.t + 1;
+  if (terminated == 0 && e.t >= S.max_steps) {
+    truncated = 1;
+    o.events |= 1u << EV_TRUNCATED_BIT;
+  }
+  e.x = x; e.y = y; e.dx = dxx; e.dy = dyy;
+  e.done = (terminated != 0 || truncated != 0) ? 1 : 0;
+  o.done = e.done;
+  o.trunc = truncated;
+  return o;
+}
+
+// ------------------------------------------------------- async bulk stores
+__device__ __forceinline__ void bulk_fence() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(gdst), "r"(s), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// --------------------------------------------------------------- rendering
+// Per-warp shared memory layout (offsets in bytes, all 16-aligned):
+//   spans: t0 u16[Wp], b0 u16[Wp], wrgb u32[Wp]   (Wp = obs_w rounded to 4)
+//   gather: dep f64[E], lat f64[E], ent i32[E]
+//   recs: SpriteRec[E]
+//   band buffers: 2 x band_stride
+struct WarpSmem {
+  uint16_t* t0;
+  uint16_t* b0;
+  uint32_t* wrgb;
+  double* gdep;
+  double* glat;
+  int* gent;
+  SpriteRec* recs;
+  uint8_t* band[2];
+};
+
+__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline int warp_smem_bytes(int obs_w, int n_ent, int band_stride) {
+  const int wp = (obs_w + 3) & ~3;
+  int off = align16(wp * 2) * 2 + align16(wp * 4);
+  const int e = n_ent > 0 ? n_ent : 1;
+  off += align16(e * 8) * 2 + align16(e * 4);
+  off += align16(e * (int)sizeof(SpriteRec));
+  off += 2 * band_stride;
+  return off;
+}
+
+__device__ inline WarpSmem carve(uint8_t* base, int obs_w, int n_ent, int band_stride) {
+  WarpSmem m;
+  const int wp = (obs_w + 3) & ~3;
+  const int e = n_ent > 0 ? n_ent : 1;
+  uint8_t* p = base;
+  m.t0 = (uint16_t*)p; p += align16(wp * 2);
+  m.b0 = (uint16_t*)p; p += align16(wp * 2);
+  m.wrgb = (uint32_t*)p; p += align16(wp * 4);
+  m.gdep = (double*)p; p += align16(e * 8);
+  m.glat = (double*)p; p += align16(e * 8);
+  m.gent = (int*)p; p += align16(e * 4);
+  m.recs = (SpriteRec*)p; p += align16(e * (int)sizeof(SpriteRec));
+  m.band[0] = p; p += band_stride;
+  m.band[1] = p;
+  return m;
+}
+
+// Render one environment's frame (all 32 lanes of the warp participate).
+// Returns the status of the first failing column (or OK), warp-uniform.
+// _pycore.py:132-271.
+template <int NC>
+__device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
+                          const WarpSmem& sm, const Env& e, uint8_t* __restrict__ frame,
+                          double* __restrict__ zbuf_out, int32_t* __restrict__ rayinfo,
+                          unsigned long long* __restrict__ spritevis_out, int& bulk_pending,
+                          int& buf) {
+  const int lane = threadIdx.x & 31;
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
+  const double atten = S.fc[FC_ATTEN];
+  const double planex = -e.dy * PLANE_HALF_WIDTH;
+  const double planey = e.dx * PLANE_HALF_WIDTH;
+
+  // ---- wall pass: one ray per column, _pycore.py:153-190
+  double zb[NC];
+  int bad_col = 0x7fffffff, bad_status = TC_ST_OK;
+#pragma unroll
+  for (int j = 0; j < NC; j++) {
+    const int c = lane + 32 * j;
+    zb[j] = 0.0;
+    if (c < W) {
+      const double k = S.coef[c];
+      const double rx = e.dx + planex * k;
+      const double ry = e.dy + planey * k;
+      const RayHit hit = cast_ray(cell, S.h, S.w, e.dmask, e.x, e.y, rx, ry);
+      if (rayinfo) {
+        rayinfo[c * 4 + 0] = hit.mapx; rayinfo[c * 4 + 1] = hit.mapy;
+        rayinfo[c * 4 + 2] = hit.side; rayinfo[c * 4 + 3] = hit.steps;
+      }
+      if (hit.status != TC_ST_OK) {
+        if (c < bad_col) { bad_col = c; bad_status = hit.status; }
+        sm.t0[c] = 0; sm.b0[c] = 0; sm.wrgb[c] = 0;
+        zb[j] = dinf();
+        continue;
+      }
+      zb[j] = hit.perp;
+      if (zbuf_out) zbuf_out[c] = hit.perp;
+      const double shade = 1.0 / (1.0 + atten * hit.perp);
+      const uint32_t cw = cell[hit.mapy * S.w + hit.mapx];
+      const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
+                                                                       : S.pal[cw & 0xffu];
+      sm.wrgb[c] = rgb_scale(base, shade);
+      double lh_f = (double)H / hit.perp;
+      if (lh_f > 1e9) lh_f = 1e9;
+      const int half = (int)lh_f / 2;
+      const int top = h2 - half, bot = h2 + half;
+      sm.t0[c] = (uint16_t)(top > 0 ? top : 0);
+      sm.b0[c] = (uint16_t)(bot < H ? bot : H);
+    }
+  }
+  // pad columns so 4-wide loads past W read harmless data
+  if (lane < ((W + 3) & ~3) - W) {
+    sm.t0[W + lane] = 0; sm.b0[W + lane] = 0; sm.wrgb[W + lane] = 0;
+  }
+  // first failing column across the warp (the reference stops there)
+  {
+    int m = bad_col;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (m != 0x7fffffff) {
+      const int src = m & 31;
+      const int st = __shfl_sync(0xffffffffu, bad_status, src);
+      __syncwarp();
+      return st;
+    }
+  }
+
+  // ---- sprite gather in entity order, _pycore.py:192-209
+  int m = 0;
+  const double det = planex * e.dy - e.dx * planey;
+  if (det != 0.0 && S.n_ent > 0) {
+    const double invdet = 1.0 / det;
+    for (int base = 0; base < S.n_ent; base += 32) {
+      const int ent = base + lane;
+      bool keep = false;
+      double lat = 0.0, dep = 0.0;
+      if (ent < S.n_ent && ((e.emask >> ent) & 1ULL) &&
+          !(S.ekind[ent] == K_GOAL && ent != e.agoal)) {
+        const double relx = S.epx[ent] - e.x;
+        const double rely = S.epy[ent] - e.y;
+        lat = invdet * (e.dy * relx - e.dx * rely);
+        dep = invdet * (-planey * relx + planex * rely);
+        keep = !(dep < S.fc[FC_MIN_SPRITE_DEPTH]);
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int slot = m + __popc(bal & ((1u << lane) - 1u));
+        sm.gdep[slot] = dep;
+        sm.glat[slot] = lat;
+        sm.gent[slot] = ent;
+      }
+      m += __popc(bal);
+    }
+  }
+  __syncwarp();
+  // stable far -> near order (= the reference's insertion sort,
+  // _pycore.py:210-217): rank = #deeper + #equal-and-earlier
+  for (int s = lane; s < m; s += 32) {
+    const double d = sm.gdep[s];
+    int rank = 0;
+    for (int j = 0; j < m; j++) {
+      const double dj = sm.gdep[j];
+      rank += (dj > d) || (dj == d && j < s);
+    }
+    // sprite parameters, _pycore.py:219-252
+    SpriteRec r;
+    const int ent = sm.gent[s];
+    r.dep = d;
+    r.ks = sm.glat[s] / d;
+    r.halfk = S.fc[FC_SPRITE_K] / d;
+    const double shade = 1.0 / (1.0 + atten * d);
+    double sh_f = (double)H / d;
+    if (sh_f > 1e9) sh_f = 1e9;
+    const int vhalf = (int)sh_f / 2;
+    r.vtop = h2 - vhalf;
+    const int vbot = h2 + vhalf;
+    r.denom = vbot - r.vtop;
+    r.r0 = r.vtop > 0 ? r.vtop : 0;
+    r.r1 = vbot < H ? vbot : H;
+    r.kd = S.ekind[ent];
+    r.ent = ent;
+    const uint32_t m1 = r.kd == K_KEY ? S.key_rgb[S.ecol[ent]]
+                        : r.kd == K_GOAL ? S.goal_rgb : S.med_cross;
+    r.s1 = rgb_scale(m1, shade);
+    r.s2 = rgb_scale(S.med_box, shade);
+    sm.recs[rank] = r;
+  }
+  __syncwarp();
+
+  if (spritevis_out) {
+    unsigned long long vis = 0;
+    for (int s = 0; s < m; s++) {
+      const SpriteRec& r = sm.recs[s];
+      if (r.denom <= 0 || r.r0 >= r.r1) continue;
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < NC; j++) {
+        const int c = lane + 32 * j;
+        if (c < W && !(zb[j] <= r.dep)) {
+          const double a = (S.coef[c] - r.ks) / r.halfk;
+          any |= !(a <= -1.0 || a >= 1.0);
+        }
+      }
+      if (__any_sync(0xffffffffu, any)) vis |= 1ULL << r.ent;
+    }
+    if (lane == 0) *spritevis_out = vis;
+  }
+
+  // ---- frame: bands of rows staged in shared memory
+  const int row_bytes = W * 3;
+  const int B = S.band_rows;
+  const uint32_t ceil_rgb = S.ceil_rgb, floor_rgb = S.floor_rgb;
+  for (int r_lo = 0; r_lo < H; r_lo += B, buf ^= 1) {
+    const int rows = min(B, H - r_lo);
+    uint8_t* band = sm.band[buf];
+    // the buffer we are about to overwrite was shipped two bands ago
+    if (S.bulk && lane == 0 && bulk_pending > 1) bulk_wait_read_le1();
+    __syncwarp();
+    if (S.quads) {
+      // 4-pixel groups: 12 bytes = 3 words, packed with PRMT
+      const int Q = W >> 2;
+      const int items = rows * Q;
+      for (int g = lane; g < items; g += 32) {
+        const int rr = g / Q, q = g - rr * Q;
+        const int row = r_lo + rr;
+        const uint2 t4 = *reinterpret_cast<const uint2*>(sm.t0 + 4 * q);
+        const uint2 b4 = *reinterpret_cast<const uint2*>(sm.b0 + 4 * q);
+        const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb + 4 * q);
+        uint32_t px[4];
+        const uint32_t tt[4] = {t4.x & 0xffffu, t4.x >> 16, t4.y & 0xffffu, t4.y >> 16};
+        const uint32_t bb[4] = {b4.x & 0xffffu, b4.x >> 16, b4.y & 0xffffu, b4.y >> 16};
+        const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          px[k] = (uint32_t)row < tt[k] ? ceil_rgb : ((uint32_t)row < bb[k] ? ww[k] : floor_rgb);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(band + rr * row_bytes + q * 12);
+        dst[0] = __byte_perm(px[0], px[1], 0x4210);
+        dst[1] = __byte_perm(px[1], px[2], 0x5421);
+        dst[2] = __byte_perm(px[2], px[3], 0x6542);
+      }
+    } else {
+      const int items = rows * W;
+      for (int p = lane; p < items; p += 32) {
+        const int rr = p / W, c = p - rr * W;
+        const uint32_t row = (uint32_t)(r_lo + rr);
+        const uint32_t col = row < sm.t0[c] ? ceil_rgb : (row < sm.b0[c] ? sm.wrgb[c] : floor_rgb);
+        uint8_t* d = band + rr * row_bytes + c * 3;
+        d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
+      }
+    }
+    __syncwarp();
+    // sprites in draw order overwrite their pixels; lane L owns columns
+    // L + 32j (the same lane that holds zbuf for them), _pycore.py:253-270
+    for (int s = 0; s < m; s++) {
+      const SpriteRec& r = sm.recs[s];
+      if (r.denom <= 0) continue;
+      const int ra = max(r.r0, r_lo), rb = min(r.r1, r_lo + rows);
+      if (ra >= rb) continue;
+      double aa[NC], ea[NC];
+      bool vis[NC];
+      bool anyvis = false;
+#pragma unroll
+      for (int j = 0; j < NC; j++) {
+        const int c = lane + 32 * j;
+        vis[j] = false;
+        aa[j] = 0.0;
+        ea[j] = 0.0;
+        if (c < W && !(zb[j] <= r.dep)) {
+          const double a = (S.coef[c] - r.ks) / r.halfk;
+          if (!(a <= -1.0 || a >= 1.0)) {
+            vis[j] = true;
+            aa[j] = a >= 0.0 ? a : -a;
+            if (r.kd == K_KEY) ea[j] = aa[j] / 0.30;
+          }
+        }
+        anyvis |= vis[j];
+      }
+      if (!__any_sync(0xffffffffu, anyvis)) continue;
+      const double denom = (double)r.denom;
+      for (int row = ra; row < rb; row++) {
+        const double v = ((double)(row - r.vtop) + 0.5) / denom;
+        const double ev = r.kd == K_KEY ? (v - 0.30) / 0.18 : 0.0;
+        uint8_t* drow = band + (row - r_lo) * row_bytes;
+#pragma unroll
+        for (int j = 0; j < NC; j++) {
+          if (!vis[j]) continue;
+          const int mk = sprite_mask(r.kd, aa[j], ea[j], v, ev);
+          if (mk) {
+            const uint32_t col = mk == 1 ? r.s1 : r.s2;
+            uint8_t* d = drow + (lane + 32 * j) * 3;
+            d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
+          }
+        }
+      }
+    }
+    // ship the band
+    const int bytes = rows * row_bytes;
+    uint8_t* gdst = frame + (size_t)r_lo * row_bytes;
+    if (S.bulk) {
+      bulk_fence();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_store(gdst, band, (uint32_t)bytes);
+        bulk_pending++;
+      }
+    } else {
+      __syncwarp();
+      for (int b = lane; b < bytes; b += 32) gdst[b] = band[b];
+    }
+  }
+  __syncwarp();
+  return TC_ST_OK;
+}
+
+// ------------------------------------------------------------- the kernels
+__device__ __forceinline__ void load_env(const SpecDev& S, const StateDev& st, long long i,
+                                         Env& e) {
+  const int lane = threadIdx.x & 31;
+  e.x = st.px[i]; e.y = st.py[i]; e.dx = st.dx[i]; e.dy = st.dy[i];
+  e.health = st.health[i];
+  e.inv = st.inv[i];
+  e.t = st.t[i];
+  e.rkey = st.rkey[i];
+  e.rctr = st.rctr[i];
+  e.done = st.done[i];
+  e.agoal = st.agoal[i];
+  const bool dop = lane < S.n_doors && st.dopen[i * S.n_doors + lane] != 0;
+  e.dmask = __ballot_sync(0xffffffffu, dop);
+  const bool a0 = lane < S.n_ent && st.ealive[i * S.n_ent + lane] != 0;
+  const bool a1 = lane + 32 < S.n_ent && st.ealive[i * S.n_ent + lane + 32] != 0;
+  e.emask = (unsigned long long)__ballot_sync(0xffffffffu, a0) |
+            ((unsigned long long)__ballot_sync(0xffffffffu, a1) << 32);
+}
+
+__device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, long long i,
+                                          const Env& e) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    st.px[i] = e.x; st.py[i] = e.y; st.dx[i] = e.dx; st.dy[i] = e.dy;
+    st.health[i] = e.health;
+    st.inv[i] = (uint8_t)e.inv;
+    st.t[i] = e.t;
+    st.rctr[i] = e.rctr;
+    st.done[i] = (uint8_t)e.done;
+    st.agoal[i] = e.agoal;
+  }
+  if (lane < S.n_doors) st.dopen[i * S.n_doors + lane] = (uint8_t)((e.dmask >> lane) & 1u);
+  if (lane < S.n_ent) st.ealive[i * S.n_ent + lane] = (uint8_t)((e.emask >> lane) & 1ULL);
+  if (lane + 32 < S.n_ent)
+    st.ealive[i * S.n_ent + lane + 32] = (uint8_t)((e.emask >> (lane + 32)) & 1ULL);
+}
+
+__device__ __forceinline__ const uint32_t* stage_map(const SpecDev& S, uint32_t* smap) {
+  if (!S.smem_map) return S.cell;
+  const int cells = S.h * S.w;
+  for (int k = threadIdx.x; k < cells; k += blockDim.x) smap[k] = S.cell[k];
+  __syncthreads();
+  return smap;
+}
+
+// MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387
+template <int NC>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
+batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutDev out,
+             long long n, int mode, int auto_reset, int validate,
+             tc_counters* __restrict__ counters) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
+  const int map_bytes = S.smem_map ? align16(S.h * S.w * 4) : 0;
+  const uint32_t* cell = stage_map(S, smap);
+  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
+                            S.band_stride);
+  const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
+  int bulk_pending = 0, buf = 0;
+  unsigned long long viol = 0;
+  uint32_t badbits = 0;
+
+  for (long long i = (long long)blockIdx.x * WARPS_PER_CTA + warp; i < n;
+       i += (long long)gridDim.x * WARPS_PER_CTA) {
+    Env e;
+    int status = TC_ST_OK;
+    if (mode == MODE_RESET) {
+      e.rkey = st.rkey[i];
+      e.rctr = st.rctr[i];
+      reset_draws(S, e);
+      store_env(S, st, i, e);
+    } else {
+      load_env(S, st, i, e);
+      if (mode == MODE_STEP) {
+        const long long act = actions[i];
+        if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
+          status = TC_ST_BAD_ACTION;
+        } else {
+          const StepOut o = step_dynamics(S, cell, e, (int)act, validate);
+          if (lane == 0) {
+            out.rewards[i] = o.reward;
+            out.dones[i] = (uint8_t)o.done;
+            out.truncs[i] = (uint8_t)o.trunc;
+            out.events[i] = o.events;
+          }
+          viol += (unsigned long long)o.violation;
+          if (o.done && auto_reset) reset_draws(S, e);
+          store_env(S, st, i, e);
+        }
+      }
+    }
+    if (status == TC_ST_OK) {
+      status = render_env<NC>(S, cell, sm, e, out.frames + (size_t)i * frame_bytes,
+                              out.zbuf ? out.zbuf + (size_t)i * S.obs_w : nullptr,
+                              out.rayinfo ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
+                              out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf);
+    }
+    if (lane == 0) out.statuses[i] = status;
+    if (status != TC_ST_OK) badbits |= 1u << status;
+  }
+  if (lane == 0) {
+    if (bulk_pending) bulk_wait_all();
+    if (counters) {
+      if (viol) atomicAdd(reinterpret_cast<unsigned long long*>(&counters->violations), viol);
+      if (badbits) atomicOr(&counters->bad_status, badbits);
+    }
+  }
+}
+
+// K fused steps with on-device policy actions (batch.py:141-153 draws) and
+// auto-reset; the env's state stays in registers across steps.
+template <int NC>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
+rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
+               tc_counters* __restrict__ counters) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
+  const int map_bytes = S.smem_map ? align16(S.h * S.w * 4) : 0;
+  const uint32_t* cell = stage_map(S, smap);
+  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
+                            S.band_stride);
+  const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
+  int bulk_pending = 0, buf = 0;
+  uint32_t badbits = 0;
+
+  for (long long i = (long long)blockIdx.x * WARPS_PER_CTA + warp; i < n;
+       i += (long long)gridDim.x * WARPS_PER_CTA) {
+    Env e;
+    int st_acc = TC_ST_OK;
+    load_env(S, st, i, e);
+    for (int k = 0; k < ra.k_steps; k++) {
+      const long long step = ra.step0 + k;
+      unsigned long long ctr = (unsigned long long)(step * ra.n_total + ra.base + i);
+      const int act = ra.tags[draw_below(ra.policy_key, ctr, (uint64_t)ra.n_tags)];
+      const StepOut o = step_dynamics(S, cell, e, act, 0);
+      const size_t kn = (size_t)k * (size_t)n + (size_t)i;
+      if (lane == 0) {
+        if (out.rewards) out.rewards[kn] = o.reward;
+        if (out.dones) out.dones[kn] = (uint8_t)o.done;
+        if (out.truncs) out.truncs[kn] = (uint8_t)o.trunc;
+        if (out.events) out.events[kn] = o.events;
+      }
+      if (o.done) reset_draws(S, e);
+      const size_t slot = (size_t)(k % ra.frame_ring) * (size_t)n + (size_t)i;
+      const int status = render_env<NC>(S, cell, sm, e, out.frames + slot * frame_bytes,
+                                        nullptr, nullptr, nullptr, bulk_pending, buf);
+      if (status != TC_ST_OK) {
+        badbits |= 1u << status;
+        if (st_acc == TC_ST_OK) st_acc = status;
+      }
+    }
+    store_env(S, st, i, e);
+    if (lane == 0 && out.statuses) out.statuses[i] = st_acc;
+  }
+  if (lane == 0) {
+    if (bulk_pending) bulk_wait_all();
+    if (counters && badbits) atomicOr(&counters->bad_status, badbits);
+  }
+}
+
+__global__ void seed_kernel(uint64_t root, long long base, long long n,
+                            unsigned long long* rkey, unsigned long long* rctr) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    rkey[i] = mix64(root + SPLIT_SALT + (uint64_t)(base + i) * GOLDEN);
+    rctr[i] = 0;
+  }
+}
+
+struct Tags { long long v[A_COUNT]; };
+
+__global__ void policy_kernel(uint64_t key, long long step, long long n_total, long long base,
+                              long long n, Tags tags, int n_tags, long long* actions) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long ctr = (unsigned long long)(step * n_total + base + i);
+    actions[i] = tags.v[draw_below(key, ctr, (uint64_t)n_tags)];
+  }
+}
+
+__global__ void cast_ray_kernel(const uint32_t* cell, int h, int w, uint32_t dmask, double ox,
+                                double oy, double rx, double ry, int32_t* io, double* dout) {
+  const RayHit r = cast_ray(cell, h, w, dmask, ox, oy, rx, ry);
+  io[0] = r.status; io[1] = r.mapx; io[2] = r.mapy; io[3] = r.side; io[4] = r.steps;
+  dout[0] = r.perp; dout[1] = r.wu;
+}
+
+}  // namespace
+
+// =================================================================== host
+struct tc_spec {
+  SpecDev dev;
+  void* blob = nullptr;
+  int nc = 1;
+  int max_ctas = 0;  // grid size for one full wave
+  size_t smem_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(TC_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define TC_CUDA(call)                                    \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+uint32_t pack_rgb(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
+}
+
+int pick_nc(int obs_w) {
+  const int need = (obs_w + 31) / 32;
+  const int opts[] = {1, 2, 3, 4, 8, 16, 32};
+  for (int o : opts)
+    if (o >= need) return o;
+  return 32;
+}
+
+template <int NC>
+const void* batch_fn() { return (const void*)batch_kernel<NC>; }
+template <int NC>
+const void* rollout_fn() { return (const void*)rollout_kernel<NC>; }
+
+const void* select_batch(int nc) {
+  switch (nc) {
+    case 1: return batch_fn<1>();
+    case 2: return batch_fn<2>();
+    case 3: return batch_fn<3>();
+    case 4: return batch_fn<4>();
+    case 8: return batch_fn<8>();
+    case 16: return batch_fn<16>();
+    default: return batch_fn<32>();
+  }
+}
+const void* select_rollout(int nc) {
+  switch (nc) {
+    case 1: return rollout_fn<1>();
+    case 2: return rollout_fn<2>();
+    case 3: return rollout_fn<3>();
+    case 4: return rollout_fn<4>();
+    case 8: return rollout_fn<8>();
+    case 16: return rollout_fn<16>();
+    default: return rollout_fn<32>();
+  }
+}
+
+// validates host tables and builds the packed cell words
+int validate_tables(const tc_tables* t, std::vector<uint32_t>& cells) {
+  if (!t) return fail(TC_E_INVALID, "tables is NULL");
+  if (t->h < 1 || t->w < 1) return fail(TC_E_INVALID, "empty map");
+  if (t->obs_w < 8 || t->obs_h < 8) return fail(TC_E_INVALID, "observation must be at least 8x8");
+  if (t->obs_w > TC_MAX_OBS_W || t->obs_h > TC_MAX_OBS_H)
+    return fail(TC_E_CAPACITY, "observation larger than TC_MAX_OBS_W/H");
+  if (t->n_entities < 0 || t->n_entities > TC_MAX_ENTITIES)
+    return fail(TC_E_CAPACITY, "too many entities");
+  if (t->n_doors < 0 || t->n_doors > TC_MAX_DOORS) return fail(TC_E_CAPACITY, "too many doors");
+  if (t->n_spawns < 1) return fail(TC_E_INVALID, "map has no spawn candidates");
+  if (t->n_pal < 1 || t->n_pal > 256) return fail(TC_E_INVALID, "palette size must be 1..256");
+  const int cells_n = t->h * t->w;
+  cells.assign(cells_n, 0);
+  for (int k = 0; k < cells_n; k++) {
+    const uint32_t tag = t->kind[k];
+    uint32_t idx = 0;
+    if (tag == C_WALL) {
+      if (t->wcol[k] >= t->n_pal) return fail(TC_E_INVALID, "wall colour outside the palette");
+      idx = t->wcol[k];
+    } else if (tag == C_DOOR) {
+      const int di = t->didx[k];
+      if (di < 0 || di >= t->n_doors) return fail(TC_E_INVALID, "door cell without a door record");
+      idx = (uint32_t)di;
+    } else if (tag != C_FLOOR) {
+      return fail(TC_E_INVALID, "cell tag must be 0 (floor), 1 (wall) or 2 (door)");
+    }
+    uint32_t eat = 0;
+    const int ei = t->eat ? t->eat[k] : -1;
+    if (ei >= 0) {
+      if (ei >= t->n_entities) return fail(TC_E_INVALID, "eat[] entity index out of range");
+      eat = (uint32_t)ei + 1;
+    }
+    cells[k] = idx | (tag << CELL_TAG_SHIFT) | (eat << CELL_EAT_SHIFT);
+  }
+  for (int d = 0; d < t->n_doors; d++)
+    if (t->dcol[d] > 2) return fail(TC_E_INVALID, "door colour must be 0..2");
+  for (int e = 0; e < t->n_entities; e++) {
+    if (t->ekind[e] > 2) return fail(TC_E_INVALID, "entity kind must be 0..2");
+    if (t->ekind[e] == K_KEY && t->ecol[e] > 2) return fail(TC_E_INVALID, "key colour must be 0..2");
+  }
+  for (int g = 0; g < t->n_goals; g++)
+    if (t->goal_ent[g] < 0 || t->goal_ent[g] >= t->n_entities)
+      return fail(TC_E_INVALID, "goal_ent index out of range");
+  return TC_OK;
+}
+
+struct BlobBuilder {
+  std::vector<uint8_t> bytes;
+  size_t add(const void* p, size_t n) {
+    const size_t off = (bytes.size() + 15) & ~(size_t)15;
+    bytes.resize(off + (n ? n : 16), 0);
+    if (n) memcpy(bytes.data() + off, p, n);
+    return off;
+  }
+};
+
+int device_sm_count() {
+  static int sms = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  });
+  return sms;
+}
+
+int launch_geometry(tc_spec* s) {
+  SpecDev& d = s->dev;
+  const int row_bytes = d.obs_w * 3;
+  d.quads = (d.obs_w % 4) == 0;
+  d.bulk = (row_bytes % 16) == 0;
+  int rows = BAND_BYTES_TARGET / row_bytes;
+  if (rows < 1) rows = 1;
+  if (rows > d.obs_h) rows = d.obs_h;
+  d.band_rows = rows;
+  d.band_stride = align16(rows * row_bytes);
+  d.warp_smem = align16(warp_smem_bytes(d.obs_w, d.n_ent, d.band_stride));
+  d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
+  const size_t map_bytes = d.smem_map ? (size_t)align16(d.h * d.w * 4) : 0;
+  s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * d.warp_smem;
+  s->nc = pick_nc(d.obs_w);
+  const void* fns[2] = {select_batch(s->nc), select_rollout(s->nc)};
+  for (const void* fn : fns)
+    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)s->smem_bytes));
+  int per_sm = 0;
+  TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[0], WARPS_PER_CTA * 32,
+                                                        s->smem_bytes));
+  if (per_sm < 1) return fail(TC_E_CAPACITY, "kernel does not fit on an SM");
+  s->max_ctas = per_sm * device_sm_count();
+  return TC_OK;
+}
+
+StateDev to_dev(const tc_state* s) {
+  StateDev d;
+  d.px = s->px; d.py = s->py; d.dx = s->dx; d.dy = s->dy; d.health = s->health;
+  d.inv = s->inv;
+  d.t = reinterpret_cast<long long*>(s->t);
+  d.rkey = reinterpret_cast<unsigned long long*>(s->rkey);
+  d.rctr = reinterpret_cast<unsigned long long*>(s->rctr);
+  d.done = s->done; d.agoal = s->agoal; d.dopen = s->dopen; d.ealive = s->ealive;
+  return d;
+}
+
+OutDev to_dev(const tc_out* o) {
+  OutDev d;
+  d.frames = o->frames; d.zbuf = o->zbuf; d.rewards = o->rewards; d.dones = o->dones;
+  d.truncs = o->truncs; d.events = o->events; d.statuses = o->statuses;
+  d.rayinfo = o->rayinfo;
+  d.spritevis = reinterpret_cast<unsigned long long*>(o->spritevis);
+  return d;
+}
+
+int grid_for(const tc_spec* s, int64_t n) {
+  const int64_t want = (n + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  return (int)(want < s->max_ctas ? want : s->max_ctas);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tc_abi_version(void) { return TC_ABI_VERSION; }
+const char* tc_last_error(void) { return g_err.c_str(); }
+const char* tc_build_info(void) {
+  return "tilecast_b200 sm_100a; fp64 --fmad=false; warps/cta=4; TMA bulk-store bands";
+}
+
+int tc_spec_create(const tc_tables* t, tc_spec** out) {
+  if (!out) return fail(TC_E_INVALID, "out is NULL");
+  *out = nullptr;
+  std::vector<uint32_t> cells;
+  int rc = validate_tables(t, cells);
+  if (rc != TC_OK) return rc;
+
+  std::vector<uint32_t> pal(t->n_pal), doorrgb(t->n_doors);
+  for (int p = 0; p < t->n_pal; p++) pal[p] = pack_rgb(t->pal + 3 * p);
+  for (int d = 0; d < t->n_doors; d++) doorrgb[d] = pack_rgb(t->door_rgb + 3 * t->dcol[d]);
+
+  BlobBuilder b;
+  const size_t o_cell = b.add(cells.data(), cells.size() * 4);
+  const size_t o_pal = b.add(pal.data(), pal.size() * 4);
+  const size_t o_door = b.add(doorrgb.data(), doorrgb.size() * 4);
+  const size_t o_dcol = b.add(t->dcol, t->n_doors);
+  const size_t o_dlock = b.add(t->dlock, t->n_doors);
+  const size_t o_epx = b.add(t->epx, t->n_entities * 8);
+  const size_t o_epy = b.add(t->epy, t->n_entities * 8);
+  const size_t o_ekind = b.add(t->ekind, t->n_entities);
+  const size_t o_ecol = b.add(t->ecol, t->n_entities);
+  const size_t o_spx = b.add(t->spx, t->n_spawns * 8);
+  const size_t o_spy = b.add(t->spy, t->n_spawns * 8);
+  const size_t o_goal = b.add(t->goal_ent, t->n_goals * 4);
+  const size_t o_coef = b.add(t->coef, t->obs_w * 8);
+
+  tc_spec* s = new tc_spec();
+  cudaError_t e = cudaMalloc(&s->blob, b.bytes.size());
+  if (e != cudaSuccess) { delete s; return cuda_fail(e, "cudaMalloc(spec)"); }
+  e = cudaMemcpy(s->blob, b.bytes.data(), b.bytes.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(s->blob); delete s; return cuda_fail(e, "cudaMemcpy(spec)"); }
+  uint8_t* base = static_cast<uint8_t*>(s->blob);
+  SpecDev& d = s->dev;
+  d.cell = (const uint32_t*)(base + o_cell);
+  d.pal = (const uint32_t*)(base + o_pal);
+  d.doorrgb = (const uint32_t*)(base + o_door);
+  d.dcol = base + o_dcol;
+  d.dlock = base + o_dlock;
+  d.epx = (const double*)(base + o_epx);
+  d.epy = (const double*)(base + o_epy);
+  d.ekind = base + o_ekind;
+  d.ecol = base + o_ecol;
+  d.spx = (const double*)(base + o_spx);
+  d.spy = (const double*)(base + o_spy);
+  d.goal_ent = (const int32_t*)(base + o_goal);
+  d.coef = (const double*)(base + o_coef);
+  for (int k = 0; k < FC_COUNT; k++) d.fc[k] = t->fc[k];
+  for (int k = 0; k < 8; k++) d.dirs[k] = t->dirs[k];
+  d.max_steps = t->ic[0];
+  d.goal_mode = (int)t->ic[1];
+  d.use_health = (int)t->ic[2];
+  d.ceil_rgb = pack_rgb(t->ceil_rgb);
+  d.floor_rgb = pack_rgb(t->floor_rgb);
+  d.goal_rgb = pack_rgb(t->goal_rgb);
+  d.med_box = pack_rgb(t->med_box);
+  d.med_cross = pack_rgb(t->med_cross);
+  for (int k = 0; k < 3; k++) d.key_rgb[k] = pack_rgb(t->key_rgb + 3 * k);
+  d.legal_mask = 0;
+  for (int a = 0; a < A_COUNT; a++)
+    if (t->legal == nullptr || t->legal[a]) d.legal_mask |= 1u << a;
+  d.h = t->h; d.w = t->w; d.n_doors = t->n_doors; d.n_ent = t->n_entities;
+  d.n_spawns = t->n_spawns; d.n_goals = t->n_goals; d.n_pal = t->n_pal;
+  d.obs_h = t->obs_h; d.obs_w = t->obs_w;
+  rc = launch_geometry(s);
+  if (rc != TC_OK) {
+    cudaFree(s->blob);
+    delete s;
+    return rc;
+  }
+  *out = s;
+  return TC_OK;
+}
+
+int tc_spec_destroy(tc_spec* s) {
+  if (!s) return TC_OK;
+  cudaError_t e = cudaFree(s->blob);
+  delete s;
+  return e == cudaSuccess ? TC_OK : cuda_fail(e, "cudaFree(spec)");
+}
+
+int tc_batch_kernel(const tc_spec* s, const tc_state* state, const int64_t* actions_dev,
+                    const tc_out* out, int64_t n, int32_t mode, int32_t auto_reset,
+                    int32_t validate, tc_counters* counters_dev, void* stream) {
+  if (!s || !state || !out) return fail(TC_E_INVALID, "NULL spec/state/out");
+  if (n < 0) return fail(TC_E_INVALID, "n must be >= 0");
+  if (mode != TC_MODE_RESET && mode != TC_MODE_STEP && mode != MODE_RENDER)
+    return fail(TC_E_INVALID, "mode must be 0 (reset) or 1 (step)");
+  if (mode == TC_MODE_STEP && (!actions_dev || !out->rewards || !out->dones || !out->truncs ||
+                               !out->events))
+    return fail(TC_E_INVALID, "step mode needs actions, rewards, dones, truncs, events");
+  if (!out->frames || !out->statuses) return fail(TC_E_INVALID, "frames and statuses are required");
+  if (n == 0) return TC_OK;
+  const SpecDev& d = s->dev;
+  if (d.bulk && (reinterpret_cast<uintptr_t>(out->frames) & 15u))
+    return fail(TC_E_INVALID, "frames must be 16-byte aligned");
+  StateDev sd = to_dev(state);
+  OutDev od = to_dev(out);
+  const int grid = grid_for(s, n);
+  const long long nn = n;
+  const long long* acts = reinterpret_cast<const long long*>(actions_dev);
+  int m = mode, ar = auto_reset, va = validate;
+  SpecDev spec = d;
+  void* args[] = {&spec, &sd, &acts, &od, (void*)&nn, &m, &ar, &va, &counters_dev};
+  TC_CUDA(cudaLaunchKernel(select_batch(s->nc), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
+                           s->smem_bytes, (cudaStream_t)stream));
+  return TC_OK;
+}
+
+int tc_rollout(const tc_spec* s, const tc_state* state, const tc_out* out, int64_t n,
+               int64_t base, int64_t n_total, uint64_t policy_key, int64_t step0,
+               int32_t k_steps, int32_t frame_ring, tc_counters* counters_dev, void* stream) {
+  if (!s || !state || !out || !out->frames) return fail(TC_E_INVALID, "NULL spec/state/out");
+  if (n < 0 || k_steps < 0 || frame_ring < 1) return fail(TC_E_INVALID, "bad n/k/ring");
+  if (n == 0 || k_steps == 0) return TC_OK;
+  if (s->dev.bulk && (reinterpret_cast<uintptr_t>(out->frames) & 15u))
+    return fail(TC_E_INVALID, "frames must be 16-byte aligned");
+  RolloutArgs ra;
+  ra.policy_key = policy_key;
+  ra.base = base;
+  ra.n_total = n_total;
+  ra.step0 = step0;
+  ra.k_steps = k_steps;
+  ra.frame_ring = frame_ring;
+  ra.n_tags = 0;
+  for (int a = 0; a < A_COUNT; a++)
+    if ((s->dev.legal_mask >> a) & 1u) ra.tags[ra.n_tags++] = a;
+  if (ra.n_tags == 0) return fail(TC_E_INVALID, "spec has no legal actions");
+  StateDev sd = to_dev(state);
+  OutDev od = to_dev(out);
+  const int grid = grid_for(s, n);
+  const long long nn = n;
+  SpecDev spec = s->dev;
+  void* args[] = {&spec, &sd, &od, (void*)&nn, &ra, &counters_dev};
+  TC_CUDA(cudaLaunchKernel(select_rollout(s->nc), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
+                           s->smem_bytes, (cudaStream_t)stream));
+  return TC_OK;
+}
+
+int tc_seed_streams(uint64_t seed, int64_t base, int64_t n, uint64_t* rkey_dev,
+                    uint64_t* rctr_dev, void* stream) {
+  if (n < 0 || (n > 0 && (!rkey_dev || !rctr_dev))) return fail(TC_E_INVALID, "bad seed args");
+  if (n == 0) return TC_OK;
+  // from_seed: the root key is mix(seed) (rng.py:36-38)
+  uint64_t x = seed;
+  x ^= x >> 30; x *= MIX1; x ^= x >> 27; x *= MIX2; x ^= x >> 31;
+  const int threads = 256;
+  const int64_t want = (n + threads - 1) / threads;
+  const int blocks = (int)(want < 4096 ? want : 4096);
+  seed_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+      x, base, n, reinterpret_cast<unsigned long long*>(rkey_dev),
+      reinterpret_cast<unsigned long long*>(rctr_dev));
+  TC_CUDA(cudaGetLastError());
+  return TC_OK;
+}
+
+int tc_policy_actions(uint64_t policy_key, int64_t step, int64_t n_total, int64_t base,
+                      int64_t n, const int64_t* action_tags_host, int32_t n_tags,
+                      int64_t* actions_dev, void* stream) {
+  if (n_tags < 1 || n_tags > A_COUNT || !action_tags_host)
+    return fail(TC_E_INVALID, "n_tags must be 1..7");
+  if (n < 0 || (n > 0 && !actions_dev)) return fail(TC_E_INVALID, "bad actions buffer");
+  if (n == 0) return TC_OK;
+  Tags tags;
+  for (int k = 0; k < A_COUNT; k++) tags.v[k] = k < n_tags ? action_tags_host[k] : 0;
+  const int threads = 256;
+  const int64_t want = (n + threads - 1) / threads;
+  const int blocks = (int)(want < 4096 ? want : 4096);
+  policy_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+      policy_key, step, n_total, base, n, tags, n_tags,
+      reinterpret_cast<long long*>(actions_dev));
+  TC_CUDA(cudaGetLastError());
+  return TC_OK;
+}
+
+// ------------------------------------------------ host-pointer parity entry
+int tc_host_cast_ray(const uint8_t* kind, const int16_t* didx, const uint8_t* dopen, int32_t h,
+                     int32_t w, double ox, double oy, double rx, double ry, int32_t* status,
+                     int32_t* mapx, int32_t* mapy, int32_t* side, double* perp, double* wall_u,
+                     int32_t* steps) {
+  if (!kind || !didx || h < 1 || w < 1) return fail(TC_E_INVALID, "bad map");
+  std::vector<uint32_t> cells(h * w);
+  uint32_t dmask = 0;
+  for (int k = 0; k < h * w; k++) {
+    const uint32_t tag = kind[k];
+    if (tag > C_DOOR) return fail(TC_E_INVALID, "cell tag must be 0..2");
+    uint32_t idx = 0;
+    if (tag == C_DOOR) {
+      if (didx[k] < 0 || didx[k] >= TC_MAX_DOORS) return fail(TC_E_INVALID, "bad door index");
+      idx = (uint32_t)didx[k];
+      if (dopen && dopen[didx[k]]) dmask |= 1u << idx;
+    }
+    cells[k] = idx | (tag << CELL_TAG_SHIFT);
+  }
+  uint32_t* dcell = nullptr;
+  int32_t* dio = nullptr;
+  double* dd = nullptr;
+  TC_CUDA(cudaMalloc(&dcell, cells.size() * 4));
+  TC_CUDA(cudaMalloc(&dio, 5 * 4));
+  TC_CUDA(cudaMalloc(&dd, 2 * 8));
+  TC_CUDA(cudaMemcpy(dcell, cells.data(), cells.size() * 4, cudaMemcpyHostToDevice));
+  cast_ray_kernel<<<1, 1>>>(dcell, h, w, dmask, ox, oy, rx, ry, dio, dd);
+  int32_t io[5];
+  double dv[2];
+  cudaError_t e = cudaMemcpy(io, dio, sizeof io, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(dv, dd, sizeof dv, cudaMemcpyDeviceToHost);
+  cudaFree(dcell);
+  cudaFree(dio);
+  cudaFree(dd);
+  if (e != cudaSuccess) return cuda_fail(e, "cast_ray");
+  *status = io[0]; *mapx = io[1]; *mapy = io[2]; *side = io[3]; *steps = io[4];
+  *perp = dv[0]; *wall_u = dv[1];
+  return TC_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// device mirror of a host state/out block for the host-pointer entry points
+struct DevBlock {
+  std::vector<void*> ptrs;
+  ~DevBlock() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  int up(T*& dst, const T* src, size_t count, bool copy) {
+    dst = nullptr;
+    if (!src) return TC_OK;
+    void* p = nullptr;
+    const size_t bytes = count ? count * sizeof(T) : 16;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(block)");
+    ptrs.push_back(p);
+    if (copy && count) {
+      e = cudaMemcpy(p, src, count * sizeof(T), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(H2D)");
+    }
+    dst = static_cast<T*>(p);
+    return TC_OK;
+  }
+};
+template <class T>
+int down(T* host, const T* dev, size_t count) {
+  if (!host || !dev || !count) return TC_OK;
+  cudaError_t e = cudaMemcpy(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? TC_OK : cuda_fail(e, "cudaMemcpy(D2H)");
+}
+}  // namespace
+
+#define TC_TRY(x)                 \
+  do {                            \
+    int _rc = (x);                \
+    if (_rc != TC_OK) return _rc; \
+  } while (0)
+
+static int host_run(const tc_tables* t, const tc_state* sh, const int64_t* acts_h,
+                    const tc_out* oh, int64_t n, int32_t mode, int32_t auto_reset,
+                    int32_t validate, int64_t* violations) {
+  tc_spec* s = nullptr;
+  TC_TRY(tc_spec_create(t, &s));
+  struct Guard {
+    tc_spec* s;
+    ~Guard() { tc_spec_destroy(s); }
+  } guard{s};
+  const size_t D = t->n_doors, E = t->n_entities, W = t->obs_w, H = t->obs_h;
+  DevBlock blk;
+  tc_state sd;
+  tc_out od;
+  TC_TRY(blk.up(sd.px, sh->px, n, true));
+  TC_TRY(blk.up(sd.py, sh->py, n, true));
+  TC_TRY(blk.up(sd.dx, sh->dx, n, true));
+  TC_TRY(blk.up(sd.dy, sh->dy, n, true));
+  TC_TRY(blk.up(sd.health, sh->health, n, true));
+  TC_TRY(blk.up(sd.inv, sh->inv, n, true));
+  TC_TRY(blk.up(sd.t, sh->t, n, true));
+  TC_TRY(blk.up(sd.rkey, sh->rkey, n, true));
+  TC_TRY(blk.up(sd.rctr, sh->rctr, n, true));
+  TC_TRY(blk.up(sd.done, sh->done, n, true));
+  TC_TRY(blk.up(sd.agoal, sh->agoal, n, true));
+  TC_TRY(blk.up(sd.dopen, sh->dopen, n * D, true));
+  TC_TRY(blk.up(sd.ealive, sh->ealive, n * E, true));
+  const int64_t* da = nullptr;
+  int64_t* dam = nullptr;
+  if (mode == TC_MODE_STEP) {
+    TC_TRY(blk.up(dam, acts_h, n, true));
+    da = dam;
+  }
+  TC_TRY(blk.up(od.frames, oh->frames, n * H * W * 3, false));
+  TC_TRY(blk.up(od.zbuf, oh->zbuf, n * W, false));
+  TC_TRY(blk.up(od.rewards, oh->rewards, n, false));
+  TC_TRY(blk.up(od.dones, oh->dones, n, false));
+  TC_TRY(blk.up(od.truncs, oh->truncs, n, false));
+  TC_TRY(blk.up(od.events, oh->events, n, false));
+  TC_TRY(blk.up(od.statuses, oh->statuses, n, false));
+  TC_TRY(blk.up(od.rayinfo, oh->rayinfo, n * W * 4, false));
+  TC_TRY(blk.up(od.spritevis, oh->spritevis, n, false));
+  tc_counters* dc = nullptr;
+  TC_CUDA(cudaMalloc(&dc, sizeof(tc_counters)));
+  blk.ptrs.push_back(dc);
+  TC_CUDA(cudaMemset(dc, 0, sizeof(tc_counters)));
+  if (od.zbuf) TC_CUDA(cudaMemset(od.zbuf, 0, n * W * 8));
+  TC_TRY(tc_batch_kernel(s, &sd, da, &od, n, mode, auto_reset, validate, dc, nullptr));
+  TC_CUDA(cudaDeviceSynchronize());
+  TC_TRY(down(sh->px, sd.px, n));
+  TC_TRY(down(sh->py, sd.py, n));
+  TC_TRY(down(sh->dx, sd.dx, n));
+  TC_TRY(down(sh->dy, sd.dy, n));
+  TC_TRY(down(sh->health, sd.health, n));
+  TC_TRY(down(sh->inv, sd.inv, n));
+  TC_TRY(down(sh->t, sd.t, n));
+  TC_TRY(down(sh->rkey, sd.rkey, n));
+  TC_TRY(down(sh->rctr, sd.rctr, n));
+  TC_TRY(down(sh->done, sd.done, n));
+  TC_TRY(down(sh->agoal, sd.agoal, n));
+  TC_TRY(down(sh->dopen, sd.dopen, n * D));
+  TC_TRY(down(sh->ealive, sd.ealive, n * E));
+  TC_TRY(down(oh->frames, od.frames, n * H * W * 3));
+  TC_TRY(down(oh->zbuf, od.zbuf, n * W));
+  TC_TRY(down(oh->rewards, od.rewards, n));
+  TC_TRY(down(oh->dones, od.dones, n));
+  TC_TRY(down(oh->truncs, od.truncs, n));
+  TC_TRY(down(oh->events, od.events, n));
+  TC_TRY(down(oh->statuses, od.statuses, n));
+  TC_TRY(down(oh->rayinfo, od.rayinfo, n * W * 4));
+  TC_TRY(down(oh->spritevis, od.spritevis, n));
+  if (violations) {
+    tc_counters hc;
+    TC_CUDA(cudaMemcpy(&hc, dc, sizeof hc, cudaMemcpyDeviceToHost));
+    *violations = (int64_t)hc.violations;
+  }
+  return TC_OK;
+}
+
+extern "C" {
+
+int tc_host_render_into(const tc_tables* t, double px, double py, double dx, double dy,
+                        const uint8_t* dopen_row, const uint8_t* ealive_row, int32_t agoal,
+                        uint8_t* frame, double* zbuf, int32_t* status) {
+  if (!t || !frame || !status) return fail(TC_E_INVALID, "NULL argument");
+  double x = px, y = py, ddx = dx, ddy = dy, health = 100.0;
+  uint8_t inv = 0, done = 0;
+  int64_t tt = 0;
+  uint64_t rkey = 0, rctr = 0;
+  int32_t ag = agoal;
+  uint8_t dop[TC_MAX_DOORS] = {0}, eal[TC_MAX_ENTITIES] = {0};
+  if (t->n_doors > TC_MAX_DOORS || t->n_entities > TC_MAX_ENTITIES)
+    return fail(TC_E_CAPACITY, "too many doors/entities");
+  for (int d = 0; d < t->n_doors; d++) dop[d] = dopen_row ? dopen_row[d] : 0;
+  for (int e = 0; e < t->n_entities; e++) eal[e] = ealive_row ? ealive_row[e] : 1;
+  tc_state s = {&x, &y, &ddx, &ddy, &health, &inv, &tt, &rkey, &rctr, &done, &ag, dop, eal};
+  std::vector<double> zb(t->obs_w, 0.0);
+  tc_out o;
+  memset(&o, 0, sizeof o);
+  o.frames = frame;
+  o.zbuf = zbuf ? zbuf : zb.data();
+  o.statuses = status;
+  return host_run(t, &s, nullptr, &o, 1, MODE_RENDER, 0, 0, nullptr);
+}
+
+int tc_host_batch_kernel(const tc_tables* t, const tc_state* state_host,
+                         const int64_t* actions_host, const tc_out* out_host, int64_t n,
+                         int32_t mode, int32_t auto_reset, int32_t validate,
+                         int64_t* violations) {
+  if (!t || !state_host || !out_host) return fail(TC_E_INVALID, "NULL argument");
+  if (mode != TC_MODE_RESET && mode != TC_MODE_STEP) return fail(TC_E_INVALID, "bad mode");
+  if (n < 0) return fail(TC_E_INVALID, "n must be >= 0");
+  if (violations) *violations = 0;
+  if (n == 0) return TC_OK;
+  return host_run(t, state_host, actions_host, out_host, n, mode, auto_reset, validate,
+                  violations);
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+"""CUDA path vs the oracle (and the reference's golden fixtures), bit-exact.
+
+Every test calls the product through its C ABI (via the host layer); the
+oracle port is only the checker. Mirrors the reference's cross-backend
+parity suite (pkg/tests/test_backends.py:40-120, test_batch.py:26-120).
+"""
+
+from __future__ import annotations
+
+import math
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, unpack_map
+from _digest import Digest
+
+import paper_2605_19926_b200 as tc
+from paper_2605_19926_b200 import layout as L
+from paper_2605_19926_b200.tables import build_tables
+from paper_2605_19926_b200.synthetic import random_tilemap
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def _assert_state(bs, ref_state, where=""):
+    host = bs.host_state()
+    for k, v in ref_state.items():
+        assert np.array_equal(host[k], v), f"{where}: state {k} differs"
+
+
+def _compare_rollout(spec, n, steps, seed, check_every=1, debug=False):
+    acts = tc.policy_actions(spec, n, steps, seed)
+    bs = tc.batch_reset(spec, n, seed, device=DEV, debug=debug)
+    r = orc.Rollout(spec, n, seed, debug=debug)
+    assert np.array_equal(bs.frames.cpu().numpy(), r.out["frames"]), "reset frames"
+    _assert_state(bs, r.state, "reset")
+    for s in range(steps):
+        bs, rew, done = tc.batch_step(bs, acts[s], reuse=True)
+        r.step(acts[s])
+        if s % check_every == 0 or s == steps - 1:
+            assert np.array_equal(rew.cpu().numpy(), r.out["rewards"]), s
+            assert np.array_equal(done.cpu().numpy(), r.out["dones"] != 0), s
+            assert np.array_equal(bs._ob.truncs.cpu().numpy(), r.out["truncs"]), s
+            assert np.array_equal(bs.last_events, r.out["events"]), s
+            fr = bs.frames.cpu().numpy()
+            if not np.array_equal(fr, r.out["frames"]):
+                bad = np.argwhere((fr != r.out["frames"]).any(axis=-1))
+                raise AssertionError(f"step {s}: {len(bad)} pixels differ, first {bad[:5]}")
+            _assert_state(bs, r.state, f"step {s}")
+            if debug:
+                assert np.array_equal(bs._ob.zbuf.cpu().numpy(), r.out["zbuf"]), s
+                assert np.array_equal(bs._ob.rayinfo.cpu().numpy(), r.out["rayinfo"]), s
+                assert np.array_equal(bs._ob.spritevis.cpu().numpy().view(np.uint64),
+                                      r.out["spritevis"]), s
+    bs.check()
+    return bs
+
+
+@pytest.mark.parametrize("env", ["simple", "key-door", "key-corridor", "health-gathering",
+                                 "my-way-home", "dmlab-static-01", "dmlab-random-goal-02",
+                                 "dmlab-static-03"])
+def test_shipped_env_rollouts_bitexact(env):
+    spec = tc.make_env(env, max_steps=45)
+    _compare_rollout(spec, 96, 120, seed=1, debug=True)
+
+
+@pytest.mark.parametrize("wh", [(64, 64), (128, 128), (8, 8), (40, 24), (37, 29), (96, 33),
+                                (256, 160)])
+def test_observation_sizes_bitexact(wh):
+    w, h = wh
+    spec = tc.make_env("health-gathering", obs_width=w, obs_height=h, max_steps=30)
+    _compare_rollout(spec, 40, 50, seed=4, debug=True)
+
+
+def test_synthetic_maps_bitexact():
+    for s in range(12):
+        tmap = random_tilemap(random.Random(1000 + s))
+        spec = tc.EnvSpec(id=f"syn{s}", map=tmap, action_set=tc.suite.STRAFE_ACTIONS,
+                          goal_mode=tc.GoalMode.RANDOM_PER_EPISODE, max_steps=25,
+                          living_reward=0.01, health_decay=1.0, health_restore=10.0)
+        _compare_rollout(spec, 64, 60, seed=s, debug=True)
+
+
+def test_golden_digests(golden_digests):
+    for case in golden_digests:
+        spec = tc.make_env(case["env"], **case["overrides"])
+        n, steps, seed = case["n"], case["steps"], case["seed"]
+        acts = tc.policy_actions(spec, n, steps, seed)
+        bs = tc.batch_reset(spec, n, seed, device=DEV)
+        d = Digest()
+        d.frames(bs.frames.cpu().numpy())
+        for s in range(steps):
+            bs, rew, done = tc.batch_step(bs, acts[s], reuse=True)
+            d.step(bs.host_state(), rew.cpu().numpy(), done.cpu().numpy(),
+                   bs._ob.truncs.cpu().numpy(), bs.last_events, bs.frames.cpu().numpy())
+        assert d.hexdigest() == case["digest"], case
+        assert d.reward_sum == case["reward_sum"] and d.dones == case["dones"]
+
+
+def test_golden_frames_render_frame():
+    g = np.load(GOLDEN / "golden_frames.npz")
+    from paper_2605_19926_b200.maps import SHIPPED_MAPS
+    for key in g.files:
+        env, sx, sy, dx, dy = key.split("|")
+        tmap = tc.parse_map(SHIPPED_MAPS[env])
+        pose = tc.Pose.looking(tc.Vec2(float(sx), float(sy)), tc.Vec2(float(dx), float(dy)))
+        assert np.array_equal(tc.render_frame(tmap, pose), g[key]), key
+
+
+def test_random_frames_render_frame():
+    g = np.load(GOLDEN / "frames_random.npz")
+    m = 0
+    while f"f{m}_frame" in g.files:
+        tmap = unpack_map(g[f"f{m}_map"])
+        exp = g[f"f{m}_frame"]
+        px, py, dx, dy = g[f"f{m}_pose"]
+        pose = tc.Pose.looking(tc.Vec2(px, py), tc.Vec2(dx, dy))
+        got = tc.render_frame(tmap, pose, exp.shape[1], exp.shape[0],
+                              door_open=[bool(v) for v in g[f"f{m}_dopen"]])
+        assert np.array_equal(got, exp), m
+        m += 1
+
+
+def test_cast_ray_dda_matches_reference_rays():
+    g = np.load(GOLDEN / "rays.npz")
+    m = 0
+    while f"m{m}_kind" in g.files:
+        kind, didx, dopen = g[f"m{m}_kind"], g[f"m{m}_didx"], g[f"m{m}_dopen"]
+        ndoor = int(didx.max()) + 1 if didx.max() >= 0 else 0
+        tmap = _map_from_arrays(kind, didx, ndoor)
+        for q, iexp, fexp in zip(g[f"m{m}_q"], g[f"m{m}_i"], g[f"m{m}_f"]):
+            hit = tc.cast_ray_dda(tmap, tc.Vec2(q[0], q[1]), tc.Vec2(q[2], q[3]),
+                                  door_open=[bool(v) for v in dopen])
+            assert (hit.cell[0], hit.cell[1], int(hit.side), hit.steps) == \
+                (int(iexp[1]), int(iexp[2]), int(iexp[3]), int(iexp[4]))
+            assert hit.perp_distance == fexp[0] and hit.wall_u == fexp[1]
+        m += 1
+
+
+def _map_from_arrays(kind, didx, ndoor):
+    doors = [None] * ndoor
+    for y, x in zip(*np.nonzero(didx >= 0)):
+        doors[int(didx[y, x])] = tc.Door((int(x), int(y)), tc.KeyColor.RED, False)
+    floor = np.argwhere(kind == 0)
+    spawn = (int(floor[0][1]), int(floor[0][0]))
+    return tc.TileMap(kind, np.zeros_like(kind), doors, [], [spawn])
+
+
+def test_scalar_api_matches_batch():
+    spec = tc.make_env("key-door")
+    n = 4
+    bs = tc.batch_reset(spec, n, seed=7, device=DEV)
+    root = tc.from_seed(7)
+    states = []
+    for i in range(n):
+        st, obs = tc.reset(spec, tc.split(root, i))
+        assert bs.state(i) == st
+        assert np.array_equal(bs.frames[i].cpu().numpy(), obs)
+        states.append(st)
+    rnd = random.Random(b"batch-vs-scalar")
+    for _ in range(40):
+        acts = [rnd.choice(spec.action_set) for _ in range(n)]
+        bs, rewards, dones = tc.batch_step(bs, [int(a) for a in acts])
+        rewards, dones = rewards.cpu().numpy(), dones.cpu().numpy()
+        for i in range(n):
+            r = tc.step(spec, states[i], acts[i])
+            assert rewards[i] == r.reward and dones[i] == r.done
+            if r.done:
+                states[i], obs = tc.reset(spec, r.state.rng)
+                assert np.array_equal(bs.frames[i].cpu().numpy(), obs)
+            else:
+                states[i] = r.state
+                assert np.array_equal(bs.frames[i].cpu().numpy(), r.observation)
+            assert bs.state(i) == states[i]
+
+
+def test_rollout_kernel_equals_batch_steps():
+    spec = tc.make_env("dmlab-random-goal-01", max_steps=20)
+    n, k, seed = 200, 37, 5
+    a = tc.batch_reset(spec, n, seed, device=DEV)
+    b = tc.batch_reset(spec, n, seed, device=DEV)
+    ring = torch.empty((k, n, 64, 64, 3), dtype=torch.uint8, device=DEV)
+    res = tc.rollout(a, k, seed, frames=ring, record=True)
+    acts = tc.policy_actions(spec, n, k, seed)
+    for s in range(k):
+        b, rew, done = tc.batch_step(b, acts[s], reuse=True)
+        assert torch.equal(res["frames"][s], b.frames), s
+        assert torch.equal(res["rewards"][s], rew), s
+        assert torch.equal(res["dones"][s] != 0, done), s
+    ha, hb = a.host_state(), b.host_state()
+    for key in ha:
+        assert np.array_equal(ha[key], hb[key]), key
+
+
+def test_rollout_continuation_and_sharding():
+    """Global env indices: two half-shards stepped separately == one batch."""
+    spec = tc.make_env("key-door", max_steps=30)
+    n, k, seed = 256, 40, 9
+    full = tc.batch_reset(spec, n, seed, device=DEV)
+    tc.rollout(full, k // 2, seed)
+    tc.rollout(full, k - k // 2, seed, step0=k // 2)
+    halves = [tc.batch_reset(spec, n // 2, seed, device=DEV, base=b, n_total=n)
+              for b in (0, n // 2)]
+    for h in halves:
+        tc.rollout(h, k, seed)
+    hf = full.host_state()
+    for j, h in enumerate(halves):
+        hh = h.host_state()
+        sl = slice(j * n // 2, (j + 1) * n // 2)
+        for key in hf:
+            assert np.array_equal(hf[key][sl], hh[key]), key
+        assert torch.equal(full.frames[sl], h.frames)
+
+
+def test_device_policy_actions_match_host_table():
+    spec = tc.make_env("health-gathering")
+    table = tc.policy_actions(spec, 1000, 4, seed=3)
+    for s in range(4):
+        row = tc.policy_actions_device(spec, s, 1000, 3, device=DEV)
+        assert np.array_equal(row.cpu().numpy(), table[s])
+        part = tc.policy_actions_device(spec, s, 300, 3, base=500, n_total=1000, device=DEV)
+        assert np.array_equal(part.cpu().numpy(), table[s, 500:800])
+
+
+def test_validate_and_contract_errors():
+    spec = tc.make_env("simple")
+    bs = tc.batch_reset(spec, 8, 0, device=DEV)
+    with pytest.raises(tc.ContractError):
+        tc.batch_step(bs, [int(tc.Action.STRAFE_LEFT)] * 8)
+    with pytest.raises(tc.ContractError):
+        tc.batch_step(bs, [0] * 7)
+    with pytest.raises(tc.ContractError):
+        tc.batch_step(bs, [9] * 8)
+    bs, _, _ = tc.batch_step(bs, [0] * 8, validate=True)
+    bad = torch.full((8,), int(tc.Action.STRAFE_LEFT), dtype=torch.int64, device=DEV)
+    bs, _, _ = tc.batch_step(bs, bad)
+    with pytest.raises(tc.ContractError):
+        bs.check()
+
+
+def test_auto_reset_reports_final_step():
+    spec = tc.make_env("simple", max_steps=2)
+    bs = tc.batch_reset(spec, 3, seed=1, device=DEV)
+    noop = [int(tc.Action.NOOP)] * 3
+    bs, _, dones = tc.batch_step(bs, noop)
+    assert not dones.any()
+    bs, _, dones = tc.batch_step(bs, noop)
+    assert dones.all() and bs.last_truncated.all() and not bs.last_terminated.any()
+    for i in range(3):
+        assert bs.state(i).t == 0 and not bs.state(i).done
+
+
+def test_large_batch_matches_oracle_sample():
+    """BASELINE C2 size (4096 envs): full bit-exact compare on every 10th step."""
+    spec = tc.make_env("my-way-home")
+    _compare_rollout(spec, 4096, 30, seed=0, check_every=10)
