@@ -1094,9 +1094,16 @@ int launch_geometry(tc_spec* s) {
   s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * d.warp_smem;
   s->nc = pick_nc(d.obs_w);
   const void* fns[2] = {select_batch(s->nc), select_rollout(s->nc)};
+  // the attribute is per function, shared by every spec: raise it to the
+  // device's opt-in maximum once instead of per spec (occupancy follows the
+  // smem each launch actually asks for)
+  int dev = 0, optin = 0;
+  TC_CUDA(cudaGetDevice(&dev));
+  TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (s->smem_bytes > (size_t)optin)
+    return fail(TC_E_CAPACITY, "per-CTA shared memory exceeds the device limit");
   for (const void* fn : fns)
-    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)s->smem_bytes));
+    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   int per_sm = 0;
   TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[0], WARPS_PER_CTA * 32,
                                                         s->smem_bytes));
