@@ -123,12 +123,16 @@ typedef struct tc_out {
 } tc_out;
 
 /* Device-side counters written by the step kernel (read lazily by the host;
- * no per-step synchronisation). */
+ * no per-step synchronisation). Passing one also enables dynamic env
+ * scheduling (warps pull env indices from next_env). One tc_counters must not
+ * be used by two launches that may run concurrently. */
 typedef struct tc_counters {
   uint64_t violations;   /* collision-invariant violations (batch.py:133)   */
-  uint32_t bad_status;   /* OR of all non-OK statuses this call             */
+  uint32_t bad_status;   /* OR of (1 << status) over all non-OK statuses    */
+  uint32_t next_env;     /* env scheduler ticket: kernel-internal, must be  */
+  uint32_t ctas_done;    /*   zero at first use; the kernel re-zeroes them  */
   uint32_t pad;
-} tc_counters;
+} tc_counters;           /* 24 bytes; allocate zeroed, reuse across calls   */
 
 typedef struct tc_spec tc_spec; /* opaque, device-resident packed tables */
 

@@ -49,7 +49,7 @@ class TcOut(C.Structure):
 
 class TcCounters(C.Structure):
     _fields_ = [("violations", C.c_uint64), ("bad_status", C.c_uint32),
-                ("pad", C.c_uint32)]
+                ("next_env", C.c_uint32), ("ctas_done", C.c_uint32), ("pad", C.c_uint32)]
 
 
 class NativeError(RuntimeError):

@@ -56,8 +56,11 @@ constexpr uint64_t MIX2 = 0x94D049BB133111EBULL;
 constexpr uint64_t SPLIT_SALT = 0x3C6EF372FE94F82AULL;
 
 constexpr int WARPS_PER_CTA = 4;
+#ifndef TC_MIN_CTAS
+#define TC_MIN_CTAS 5  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr int BAND_BYTES_TARGET = 3072;       // per staging buffer
-constexpr int SMEM_MAP_MAX_CELLS = 8192;      // stage map in smem up to this
+constexpr int SMEM_MAP_MAX_CELLS = 4096;      // stage map in smem up to this
 
 // packed cell word: bits 0-7 = wall colour or door index, 8-9 = cell tag,
 // 16-23 = entity index + 1 (0 = no entity on the tile)
@@ -67,6 +70,7 @@ constexpr uint32_t CELL_EAT_SHIFT = 16;
 // ------------------------------------------------------------- device spec
 struct SpecDev {
   const uint32_t* cell;     // [h*w] packed cells
+  const uint32_t* solid;    // [h*w] stop codes: wall ~0u, door d 1u<<d, floor 0
   const uint32_t* pal;      // [n_pal] wall colours, r | g<<8 | b<<16
   const uint32_t* doorrgb;  // [D] door_rgb[dcol[d]]
   const uint8_t* dcol;      // [D]
@@ -92,6 +96,9 @@ struct SpecDev {
   int smem_map;      // 1 = stage cells into shared memory
   int quads;         // 1 = obs_w % 4 == 0 (4-pixel packed compose)
   int bulk;          // 1 = frame rows are 16-byte multiples (TMA bulk store)
+  int sealed;        // 1 = map rim is all wall (rays cannot escape)
+  int mirror;        // 1 = mirrored-band SWAR compose (even H <= 254, W % 16 == 0)
+  int mir_rpi;       // rows per warp pass in the mirror compose (32 / (W/16), >= 1)
   int warp_smem;     // bytes of per-warp shared memory
 };
 
@@ -267,47 +274,28 @@ __device__ __forceinline__ int sprite_mask(int kd, double aa, double ea, double 
   return 0;
 }
 
-// _pycore.py:274-304 (disc vs grid, strict <)
-__device__ __forceinline__ bool blocked(const SpecDev& S, const uint32_t* __restrict__ cell,
-                                        uint32_t dmask, double cx, double cy, double radius) {
-  const int tx0 = (int)floor(cx - radius), tx1 = (int)floor(cx + radius);
-  const int ty0 = (int)floor(cy - radius), ty1 = (int)floor(cy + radius);
-  const double r2 = radius * radius;
-  for (int ty = ty0; ty <= ty1; ty++) {
-    for (int tx = tx0; tx <= tx1; tx++) {
-      if (tx < 0 || tx >= S.w || ty < 0 || ty >= S.h) return true;
-      const uint32_t cw = cell[ty * S.w + tx];
-      const uint32_t tag = (cw >> CELL_TAG_SHIFT) & 3u;
-      if (tag == C_FLOOR) continue;
-      if (tag == C_DOOR && ((dmask >> (cw & 31u)) & 1u) != 0) continue;
-      double nx = cx;
-      if (nx < tx) nx = tx;
-      else if (nx > tx + 1.0) nx = tx + 1.0;
-      double ny = cy;
-      if (ny < ty) ny = ty;
-      else if (ny > ty + 1.0) ny = ty + 1.0;
-      const double ddx = cx - nx, ddy = cy - ny;
-      if (ddx * ddx + ddy * ddy < r2) return true;
-    }
-  }
-  return false;
-}
-
-// _pycore.py:307-343
-__device__ __forceinline__ uint32_t touch_doors(const SpecDev& S, const uint32_t* __restrict__ cell,
-                                                uint32_t& dmask, double cx, double cy,
-                                                double radius, uint32_t inv) {
+// One pass over the <= 2x2 tiles the disc (cx, cy, radius) overlaps, doing
+// _touch_doors (_pycore.py:307-343; only when `touch`) and then _blocked
+// (:274-304) for each tile. Equivalent to the reference's two passes: a
+// door's open flag only affects its own tile (one door record per door
+// cell), and touch never skips a tile that blocked would test. Returns the
+// door events; `blk` = blocked after the doors were touched.
+__device__ __noinline__ uint32_t scan_tiles(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                            const uint32_t* __restrict__ solid, uint32_t& dmask,
+                                            double cx, double cy, double radius, uint32_t inv,
+                                            bool touch, bool& blk) {
   uint32_t events = 0;
+  bool b = false;
   const int tx0 = (int)floor(cx - radius), tx1 = (int)floor(cx + radius);
   const int ty0 = (int)floor(cy - radius), ty1 = (int)floor(cy + radius);
   const double r2 = radius * radius;
+#pragma unroll 1
   for (int ty = ty0; ty <= ty1; ty++) {
+#pragma unroll 1
     for (int tx = tx0; tx <= tx1; tx++) {
-      if (tx < 0 || tx >= S.w || ty < 0 || ty >= S.h) continue;
-      const uint32_t cw = cell[ty * S.w + tx];
-      if (((cw >> CELL_TAG_SHIFT) & 3u) != C_DOOR) continue;
-      const int di = (int)(cw & 31u);
-      if ((dmask >> di) & 1u) continue;
+      if (tx < 0 || tx >= S.w || ty < 0 || ty >= S.h) { b = true; continue; }
+      const uint32_t code = solid[ty * S.w + tx];
+      if (code == 0u) continue;  // floor
       double nx = cx;
       if (nx < tx) nx = tx;
       else if (nx > tx + 1.0) nx = tx + 1.0;
@@ -315,18 +303,24 @@ __device__ __forceinline__ uint32_t touch_doors(const SpecDev& S, const uint32_t
       if (ny < ty) ny = ty;
       else if (ny > ty + 1.0) ny = ty + 1.0;
       const double ddx = cx - nx, ddy = cy - ny;
-      if (ddx * ddx + ddy * ddy >= r2) continue;
-      const int dc = S.dcol[di];
-      if (S.dlock[di] != 0 && ((inv >> dc) & 1u) == 0) continue;
-      dmask |= 1u << di;
-      events |= 1u << (EV_DOOR_BASE_BIT + dc);
+      if (!(ddx * ddx + ddy * ddy < r2)) continue;  // no overlap
+      if (code != 0xffffffffu && (code & ~dmask) != 0u && touch) {  // closed door
+        const int di = (int)(cell[ty * S.w + tx] & 31u);
+        const int dc = S.dcol[di];
+        if (!(S.dlock[di] != 0 && ((inv >> dc) & 1u) == 0)) {
+          dmask |= 1u << di;
+          events |= 1u << (EV_DOOR_BASE_BIT + dc);
+        }
+      }
+      if ((code & ~dmask) != 0u || code == 0xffffffffu) b = true;
     }
   }
+  blk = b;
   return events;
 }
 
 // _pycore.py:390-414: draws in the contract order spawn, heading, goal
-__device__ __forceinline__ void reset_draws(const SpecDev& S, Env& e) {
+__device__ __noinline__ void reset_draws(const SpecDev& S, Env& e) {
   unsigned long long ctr = e.rctr;
   uint64_t v = draw_below(e.rkey, ctr, (uint64_t)S.n_spawns);
   e.x = S.spx[v];
@@ -359,7 +353,8 @@ struct StepOut {
 
 // _pycore.py:431-531 (everything before the render / auto-reset branch)
 __device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_t* __restrict__ cell,
-                                                 Env& e, int act, int validate) {
+                                                 const uint32_t* __restrict__ solid, Env& e,
+                                                 int act, int validate) {
   StepOut o;
   o.events = 0;
   o.reward = 0.0;
@@ -381,13 +376,18 @@ __device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_
     else if (act == A_BACKWARD) { mvx = -ms * dxx; mvy = -ms * dyy; }
     else if (act == A_STRAFE_LEFT) { mvx = ms * dyy; mvy = -ms * dxx; }
     else if (act == A_STRAFE_RIGHT) { mvx = -ms * dyy; mvy = ms * dxx; }
-    const double nx = x + mvx;
-    o.events |= touch_doors(S, cell, e.dmask, nx, y, radius, e.inv);
-    if (!blocked(S, cell, e.dmask, nx, y, radius)) x = nx;
-    const double ny = y + mvy;
-    o.events |= touch_doors(S, cell, e.dmask, x, ny, radius, e.inv);
-    if (!blocked(S, cell, e.dmask, x, ny, radius)) y = ny;
-    if (validate && blocked(S, cell, e.dmask, x, y, radius)) o.violation = 1;
+    // slide: resolve x then y; contact opens doors first (_pycore.py:476-488)
+#pragma unroll 1
+    for (int ax = 0; ax < 3; ax++) {
+      if (ax == 2 && !validate) break;
+      const double cx = ax == 0 ? x + mvx : x;
+      const double cy = ax == 1 ? y + mvy : y;
+      bool blk;
+      o.events |= scan_tiles(S, cell, solid, e.dmask, cx, cy, radius, e.inv, ax < 2, blk);
+      if (ax == 0 && !blk) x = cx;
+      if (ax == 1 && !blk) y = cy;
+      if (ax == 2 && blk) o.violation = 1;
+    }
   }
   // pickups on the agent-centre tile only, _pycore.py:490-507
   const int ctx = (int)floor(x), cty = (int)floor(y);
@@ -437,11 +437,23 @@ __device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_
 __device__ __forceinline__ void bulk_fence() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+__device__ __forceinline__ void bulk_copy(void* gdst, const void* ssrc, uint32_t bytes) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                :: "l"(gdst), "r"(s), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  bulk_copy(gdst, ssrc, bytes);
+  bulk_commit();
+}
+// byte permute with per-byte sign replication (selector nibble bit 3)
+__device__ __forceinline__ uint32_t prmt_sx(uint32_t a, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(a), "r"(sel));
+  return d;
 }
 __device__ __forceinline__ void bulk_wait_read_le1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -452,30 +464,32 @@ __device__ __forceinline__ void bulk_wait_all() {
 
 // --------------------------------------------------------------- rendering
 // Per-warp shared memory layout (offsets in bytes, all 16-aligned):
-//   spans: t0 u16[Wp], b0 u16[Wp], wrgb u32[Wp]   (Wp = obs_w rounded to 4)
+//   spans: t0 u16[Wp], b0 u16[Wp], wrgb u32[Wp], zbuf f64[Wp]  (Wp = obs_w rounded to 4)
 //   gather: dep f64[E], lat f64[E], ent i32[E]
 //   recs: SpriteRec[E]
 //   band buffers: 2 x band_stride
 struct WarpSmem {
   uint16_t* t0;
   uint16_t* b0;
+  uint8_t* t8;  // t0 as bytes (mirror path, obs_h <= 254)
   uint32_t* wrgb;
+  double* zbuf;
   double* gdep;
   double* glat;
   int* gent;
   SpriteRec* recs;
-  uint8_t* band[2];
+  uint8_t* band[4];
 };
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
 __host__ __device__ inline int warp_smem_bytes(int obs_w, int n_ent, int band_stride) {
   const int wp = (obs_w + 3) & ~3;
-  int off = align16(wp * 2) * 2 + align16(wp * 4);
+  int off = align16(wp * 2) * 2 + align16(wp) + align16(wp * 4) + align16(wp * 8);
   const int e = n_ent > 0 ? n_ent : 1;
   off += align16(e * 8) * 2 + align16(e * 4);
   off += align16(e * (int)sizeof(SpriteRec));
-  off += 2 * band_stride;
+  off += 4 * band_stride;
   return off;
 }
 
@@ -486,90 +500,180 @@ __device__ inline WarpSmem carve(uint8_t* base, int obs_w, int n_ent, int band_s
   uint8_t* p = base;
   m.t0 = (uint16_t*)p; p += align16(wp * 2);
   m.b0 = (uint16_t*)p; p += align16(wp * 2);
+  m.t8 = p; p += align16(wp);
   m.wrgb = (uint32_t*)p; p += align16(wp * 4);
+  m.zbuf = (double*)p; p += align16(wp * 8);
   m.gdep = (double*)p; p += align16(e * 8);
   m.glat = (double*)p; p += align16(e * 8);
   m.gent = (int*)p; p += align16(e * 4);
   m.recs = (SpriteRec*)p; p += align16(e * (int)sizeof(SpriteRec));
-  m.band[0] = p; p += band_stride;
-  m.band[1] = p;
+  for (int k = 0; k < 4; k++) { m.band[k] = p; p += band_stride; }
   return m;
 }
 
-// Render one environment's frame (all 32 lanes of the warp participate).
-// Returns the status of the first failing column (or OK), warp-uniform.
-// _pycore.py:132-271.
-template <int NC>
-__device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
-                          const WarpSmem& sm, const Env& e, uint8_t* __restrict__ frame,
-                          double* __restrict__ zbuf_out, int32_t* __restrict__ rayinfo,
-                          unsigned long long* __restrict__ spritevis_out, int& bulk_pending,
-                          int& buf) {
-  const int lane = threadIdx.x & 31;
-  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
-  const double atten = S.fc[FC_ATTEN];
-  const double planex = -e.dy * PLANE_HALF_WIDTH;
-  const double planey = e.dx * PLANE_HALF_WIDTH;
-
-  // ---- wall pass: one ray per column, _pycore.py:153-190
-  double zb[NC];
-  int bad_col = 0x7fffffff, bad_status = TC_ST_OK;
+__device__ __forceinline__ int warp_min(int v) {
 #pragma unroll
-  for (int j = 0; j < NC; j++) {
-    const int c = lane + 32 * j;
-    zb[j] = 0.0;
-    if (c < W) {
-      const double k = S.coef[c];
-      const double rx = e.dx + planex * k;
-      const double ry = e.dy + planey * k;
-      const RayHit hit = cast_ray(cell, S.h, S.w, e.dmask, e.x, e.y, rx, ry);
-      if (rayinfo) {
-        rayinfo[c * 4 + 0] = hit.mapx; rayinfo[c * 4 + 1] = hit.mapy;
-        rayinfo[c * 4 + 2] = hit.side; rayinfo[c * 4 + 3] = hit.steps;
-      }
-      if (hit.status != TC_ST_OK) {
-        if (c < bad_col) { bad_col = c; bad_status = hit.status; }
-        sm.t0[c] = 0; sm.b0[c] = 0; sm.wrgb[c] = 0;
-        zb[j] = dinf();
-        continue;
-      }
-      zb[j] = hit.perp;
-      if (zbuf_out) zbuf_out[c] = hit.perp;
-      const double shade = 1.0 / (1.0 + atten * hit.perp);
-      const uint32_t cw = cell[hit.mapy * S.w + hit.mapx];
-      const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
-                                                                       : S.pal[cw & 0xffu];
-      sm.wrgb[c] = rgb_scale(base, shade);
-      double lh_f = (double)H / hit.perp;
-      if (lh_f > 1e9) lh_f = 1e9;
-      const int half = (int)lh_f / 2;
-      const int top = h2 - half, bot = h2 + half;
-      sm.t0[c] = (uint16_t)(top > 0 ? top : 0);
-      sm.b0[c] = (uint16_t)(bot < H ? bot : H);
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One DDA march, _pycore.py:38-96. `solid` holds per-cell stop codes
+// (wall = ~0u, door d = 1u << d, floor = 0): a ray stops in a cell iff
+// (code & ~dmask) != 0 or code == ~0u (walls, closed doors). With a sealed
+// rim and the origin inside the grid a ray can neither escape nor exceed
+// the 2(w+h) budget (it crosses at most w+h-2 boundaries before the rim),
+// so CHECKED=false drops those tests; the result is identical.
+struct March {
+  double sdx, sdy, ddx, ddy;
+  int idx, steps, status;
+  bool xs;  // last step was an x step (side 0)
+};
+
+__device__ __forceinline__ bool stops(uint32_t code, uint32_t dmask) {
+  return (code & ~dmask) != 0u || code == 0xffffffffu;
+}
+
+template <bool CHECKED>
+__device__ __forceinline__ March march(const uint32_t* __restrict__ solid, int mw, int mh,
+                                       uint32_t dmask, double ox, double oy, int mapx0,
+                                       int mapy0, double rx, double ry) {
+  March r;
+  int stepx, stepy;
+  if (rx != 0.0) {
+    r.ddx = fabs(1.0 / rx);
+    stepx = rx > 0.0 ? 1 : -1;
+    r.sdx = rx > 0.0 ? (((double)mapx0 + 1.0) - ox) * r.ddx : (ox - (double)mapx0) * r.ddx;
+  } else {
+    r.ddx = dinf(); stepx = 0; r.sdx = dinf();
+  }
+  if (ry != 0.0) {
+    r.ddy = fabs(1.0 / ry);
+    stepy = ry > 0.0 ? 1 : -1;
+    r.sdy = ry > 0.0 ? (((double)mapy0 + 1.0) - oy) * r.ddy : (oy - (double)mapy0) * r.ddy;
+  } else {
+    r.ddy = dinf(); stepy = 0; r.sdy = dinf();
+  }
+  const int dyi = stepy * mw;
+  int idx = mapy0 * mw + mapx0;
+  int steps = 0;
+  bool xs = false;
+  if (!CHECKED) {
+    for (;;) {
+      xs = r.sdx < r.sdy;  // ties step Y (_pycore.py:70)
+      if (xs) { r.sdx += r.ddx; idx += stepx; } else { r.sdy += r.ddy; idx += dyi; }
+      steps += 1;
+      if (stops(solid[idx], dmask)) break;
     }
+    r.status = TC_ST_OK;
+  } else {
+    int mapx = mapx0, mapy = mapy0;
+    const int limit = 2 * (mw + mh);
+    r.status = TC_ST_OK;
+    for (;;) {
+      xs = r.sdx < r.sdy;
+      if (xs) { r.sdx += r.ddx; mapx += stepx; } else { r.sdy += r.ddy; mapy += stepy; }
+      steps += 1;
+      if (steps > limit) { r.status = TC_ST_STEP_BUDGET; break; }
+      if ((unsigned)mapx >= (unsigned)mw || (unsigned)mapy >= (unsigned)mh) {
+        r.status = TC_ST_ESCAPED;
+        break;
+      }
+      idx = mapy * mw + mapx;
+      if (stops(solid[idx], dmask)) break;
+    }
+    // escaped / budget: report the out-of-grid cell like the reference
+    if (r.status != TC_ST_OK) idx = mapy * mw + mapx;
+    if (r.status != TC_ST_OK) { r.steps = steps; r.xs = xs; r.idx = idx;
+      r.sdx = (double)mapx; r.sdy = (double)mapy; return r; }
+  }
+  r.idx = idx;
+  r.steps = steps;
+  r.xs = xs;
+  return r;
+}
+
+// Wall pass: lane L casts the rays of columns L + 32j; per-column spans,
+// colours and zbuf go to shared memory (_pycore.py:153-190). Returns the
+// status of the first failing column (warp-uniform).
+template <int NC, bool CHECKED>
+__device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                         const uint32_t* __restrict__ solid,
+                                         const WarpSmem& sm, const Env& e, double planex,
+                                         double planey, double* __restrict__ zbuf_out,
+                                         int32_t* __restrict__ rayinfo) {
+  const int lane = threadIdx.x & 31;
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2, mw = S.w;
+  const int ox = (int)floor(e.x), oy = (int)floor(e.y);
+  const double atten = S.fc[FC_ATTEN];
+  int bad_col = 0x7fffffff, bad_status = TC_ST_OK;
+#pragma unroll 1
+  for (int c = lane; c < W; c += 32) {
+    const double k = S.coef[c];
+    const double rx = e.dx + planex * k;
+    const double ry = e.dy + planey * k;
+    const March r = march<CHECKED>(solid, mw, S.h, e.dmask, e.x, e.y, ox, oy, rx, ry);
+    if (rayinfo) {
+      int mx, my;
+      if (CHECKED && r.status != TC_ST_OK) { mx = (int)r.sdx; my = (int)r.sdy; }
+      else { my = r.idx / mw; mx = r.idx - my * mw; }
+      rayinfo[c * 4 + 0] = mx; rayinfo[c * 4 + 1] = my;
+      rayinfo[c * 4 + 2] = r.xs ? 0 : 1; rayinfo[c * 4 + 3] = r.steps;
+    }
+    if (CHECKED && r.status != TC_ST_OK) {
+      if (c < bad_col) { bad_col = c; bad_status = r.status; }
+      continue;
+    }
+    const double perp = r.xs ? r.sdx - r.ddx : r.sdy - r.ddy;
+    sm.zbuf[c] = perp;
+    if (zbuf_out) zbuf_out[c] = perp;
+    // _pycore.py:162-178
+    const double shade = 1.0 / (1.0 + atten * perp);
+    const uint32_t cw = cell[r.idx];
+    const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
+                                                                     : S.pal[cw & 0xffu];
+    sm.wrgb[c] = rgb_scale(base, shade);
+    double lh_f = (double)H / perp;
+    if (lh_f > 1e9) lh_f = 1e9;
+    const int half = (int)lh_f / 2;
+    const int top = h2 - half, bot = h2 + half;
+    sm.t0[c] = (uint16_t)(top > 0 ? top : 0);
+    sm.t8[c] = (uint8_t)(top > 0 ? top : 0);
+    sm.b0[c] = (uint16_t)(bot < H ? bot : H);
   }
   // pad columns so 4-wide loads past W read harmless data
   if (lane < ((W + 3) & ~3) - W) {
-    sm.t0[W + lane] = 0; sm.b0[W + lane] = 0; sm.wrgb[W + lane] = 0;
+    sm.t0[W + lane] = (uint16_t)h2; sm.b0[W + lane] = (uint16_t)h2; sm.wrgb[W + lane] = 0;
   }
-  // first failing column across the warp (the reference stops there)
-  {
-    int m = bad_col;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (m != 0x7fffffff) {
-      const int src = m & 31;
-      const int st = __shfl_sync(0xffffffffu, bad_status, src);
-      __syncwarp();
-      return st;
-    }
-  }
+  if (!CHECKED) return TC_ST_OK;
+  const int first_bad = warp_min(bad_col);
+  if (first_bad == 0x7fffffff) return TC_ST_OK;
+  return __shfl_sync(0xffffffffu, bad_status, first_bad & 31);
+}
 
-  // ---- sprite gather in entity order, _pycore.py:192-209
+// Sprite gather (entity order, _pycore.py:192-209) and per-sprite
+// parameters (:219-252). Sprites that provably draw nothing -- denom <= 0,
+// an empty row span, or no column with zbuf[c] > dep and |a| < 1 (the
+// reference's own per-column tests, evaluated exactly) -- are dropped
+// here; the survivors keep their relative order, so the stable far->near
+// sort (= the reference's insertion sort, :210-217) of the survivors is the
+// reference's order restricted to sprites that draw. Returns the survivor
+// count m; records land in sm.recs[0..m) in draw order.
+__device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm, const Env& e,
+                                            double planex, double planey,
+                                            unsigned long long* __restrict__ spritevis_out) {
+  const int lane = threadIdx.x & 31;
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
   int m = 0;
+  unsigned long long vis = 0;
   const double det = planex * e.dy - e.dx * planey;
-  if (det != 0.0 && S.n_ent > 0) {
+  if (det != 0.0) {
     const double invdet = 1.0 / det;
+    const double atten = S.fc[FC_ATTEN], spk = S.fc[FC_SPRITE_K];
     for (int base = 0; base < S.n_ent; base += 32) {
       const int ent = base + lane;
       bool keep = false;
@@ -582,156 +686,336 @@ __device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
         dep = invdet * (-planey * relx + planex * rely);
         keep = !(dep < S.fc[FC_MIN_SPRITE_DEPTH]);
       }
-      const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const int slot = m + __popc(bal & ((1u << lane) - 1u));
-        sm.gdep[slot] = dep;
-        sm.glat[slot] = lat;
-        sm.gent[slot] = ent;
+      uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      while (bal) {  // warp-uniform walk over the gathered sprites
+        const int src = __ffs(bal) - 1;
+        bal &= bal - 1u;
+        const double d = __shfl_sync(0xffffffffu, dep, src);
+        const double l = __shfl_sync(0xffffffffu, lat, src);
+        double sh_f = (double)H / d;
+        if (sh_f > 1e9) sh_f = 1e9;
+        const int vhalf = (int)sh_f / 2;
+        const int vtop = h2 - vhalf, vbot = h2 + vhalf;
+        const int r0 = vtop > 0 ? vtop : 0, r1 = vbot < H ? vbot : H;
+        if (vbot - vtop <= 0 || r0 >= r1) continue;
+        const double ks = l / d;
+        const double halfk = spk / d;
+        bool any = false;
+        for (int c = lane; c < W; c += 32) {
+          if (!(sm.zbuf[c] <= d)) {
+            const double a = (S.coef[c] - ks) / halfk;
+            any |= !(a <= -1.0 || a >= 1.0);
+          }
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        const int en = base + src;
+        if (lane == 0) {
+          SpriteRec r;
+          r.dep = d;
+          r.ks = ks;
+          r.halfk = halfk;
+          r.vtop = vtop;
+          r.denom = vbot - vtop;
+          r.r0 = r0;
+          r.r1 = r1;
+          r.kd = S.ekind[en];
+          r.ent = en;
+          const double shade = 1.0 / (1.0 + atten * d);
+          const uint32_t m1 = r.kd == K_KEY ? S.key_rgb[S.ecol[en]]
+                              : r.kd == K_GOAL ? S.goal_rgb : S.med_cross;
+          r.s1 = rgb_scale(m1, shade);
+          r.s2 = rgb_scale(S.med_box, shade);
+          sm.gdep[m] = d;
+          sm.recs[m] = r;  // gathered (entity) order
+        }
+        vis |= 1ULL << en;
+        m++;
       }
-      m += __popc(bal);
     }
   }
-  __syncwarp();
-  // stable far -> near order (= the reference's insertion sort,
-  // _pycore.py:210-217): rank = #deeper + #equal-and-earlier
-  for (int s = lane; s < m; s += 32) {
-    const double d = sm.gdep[s];
+  if (spritevis_out && lane == 0) *spritevis_out = vis;
+  if (m > 1) {
+    // stable far -> near: rank = #deeper + #equal-and-earlier; permute via
+    // registers (all lanes read before any lane writes)
+    __syncwarp();
+    SpriteRec mine;
     int rank = 0;
-    for (int j = 0; j < m; j++) {
-      const double dj = sm.gdep[j];
-      rank += (dj > d) || (dj == d && j < s);
+    if (lane < m) {
+      mine = sm.recs[lane];
+      const double d = sm.gdep[lane];
+      for (int j = 0; j < m; j++) {
+        const double dj = sm.gdep[j];
+        rank += (dj > d) || (dj == d && j < lane);
+      }
     }
-    // sprite parameters, _pycore.py:219-252
-    SpriteRec r;
-    const int ent = sm.gent[s];
-    r.dep = d;
-    r.ks = sm.glat[s] / d;
-    r.halfk = S.fc[FC_SPRITE_K] / d;
-    const double shade = 1.0 / (1.0 + atten * d);
-    double sh_f = (double)H / d;
-    if (sh_f > 1e9) sh_f = 1e9;
-    const int vhalf = (int)sh_f / 2;
-    r.vtop = h2 - vhalf;
-    const int vbot = h2 + vhalf;
-    r.denom = vbot - r.vtop;
-    r.r0 = r.vtop > 0 ? r.vtop : 0;
-    r.r1 = vbot < H ? vbot : H;
-    r.kd = S.ekind[ent];
-    r.ent = ent;
-    const uint32_t m1 = r.kd == K_KEY ? S.key_rgb[S.ecol[ent]]
-                        : r.kd == K_GOAL ? S.goal_rgb : S.med_cross;
-    r.s1 = rgb_scale(m1, shade);
-    r.s2 = rgb_scale(S.med_box, shade);
-    sm.recs[rank] = r;
-  }
-  __syncwarp();
-
-  if (spritevis_out) {
-    unsigned long long vis = 0;
-    for (int s = 0; s < m; s++) {
-      const SpriteRec& r = sm.recs[s];
-      if (r.denom <= 0 || r.r0 >= r.r1) continue;
-      bool any = false;
-#pragma unroll
-      for (int j = 0; j < NC; j++) {
-        const int c = lane + 32 * j;
-        if (c < W && !(zb[j] <= r.dep)) {
-          const double a = (S.coef[c] - r.ks) / r.halfk;
-          any |= !(a <= -1.0 || a >= 1.0);
+    __syncwarp();
+    if (lane < m) sm.recs[rank] = mine;
+    // m > 32 survivors: rare (capacity 64); sort the tail serially
+    if (m > 32) {
+      __syncwarp();
+      if (lane == 0) {
+        for (int i = 1; i < m; i++) {
+          const SpriteRec it = sm.recs[i];
+          int j = i;
+          while (j > 0 && sm.recs[j - 1].dep < it.dep) { sm.recs[j] = sm.recs[j - 1]; j--; }
+          sm.recs[j] = it;
         }
       }
-      if (__any_sync(0xffffffffu, any)) vis |= 1ULL << r.ent;
     }
-    if (lane == 0) *spritevis_out = vis;
+  }
+  __syncwarp();
+  return m;
+}
+
+// Sprites in draw order overwrite their pixels of the staged band(s); lane
+// L owns columns L + 32j (_pycore.py:253-270). bandB (may be NULL) is a
+// second band of the same height (the mirrored bottom band). Per-column
+// terms (a, |a|, key ellipse x) and per-row terms (v, key ellipse y) are
+// computed once per band; the mask comparisons are the reference's.
+__device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& sm, int m,
+                                          uint8_t* bandA, int rA, uint8_t* bandB, int rB,
+                                          int rows) {
+  const int lane = threadIdx.x & 31;
+  const int W = S.obs_w, row_bytes = W * 3;
+  for (int s = 0; s < m; s++) {
+    const SpriteRec r = sm.recs[s];
+    const double denom = (double)r.denom;
+    for (int half = 0; half < 2; half++) {
+      uint8_t* band = half ? bandB : bandA;
+      const int r_lo = half ? rB : rA;
+      if (band == nullptr) continue;
+      const int ra = max(r.r0, r_lo), rb = min(r.r1, r_lo + rows);
+      if (ra >= rb) continue;
+      for (int c0 = 0; c0 < W; c0 += 32) {
+        const int c = c0 + lane;
+        bool vis = false;
+        double aa = 0.0, ea = 0.0;
+        if (c < W && !(sm.zbuf[c] <= r.dep)) {
+          const double a = (S.coef[c] - r.ks) / r.halfk;
+          if (!(a <= -1.0 || a >= 1.0)) {
+            vis = true;
+            aa = a >= 0.0 ? a : -a;
+            if (r.kd == K_KEY) ea = aa / 0.30;
+          }
+        }
+        if (!__any_sync(0xffffffffu, vis)) continue;
+        for (int row = ra; row < rb; row++) {
+          const double v = ((double)(row - r.vtop) + 0.5) / denom;
+          const double ev = r.kd == K_KEY ? (v - 0.30) / 0.18 : 0.0;
+          if (!vis) continue;
+          const int mk = sprite_mask(r.kd, aa, ea, v, ev);
+          if (mk) {
+            const uint32_t col = mk == 1 ? r.s1 : r.s2;
+            uint8_t* d = band + (row - r_lo) * row_bytes + c * 3;
+            d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
+          }
+        }
+      }
+    }
+  }
+}
+
+// per-lane compose geometry, computed once per kernel (no divisions per env)
+struct LaneGeo {
+  int rowoff, cg0;
+};
+__device__ __forceinline__ LaneGeo lane_geo(const SpecDev& S) {
+  const int lane = threadIdx.x & 31;
+  const int CG = S.obs_w >> 4;
+  LaneGeo g;
+  g.rowoff = (S.mirror && CG < 32) ? lane / CG : 0;
+  g.cg0 = (S.mirror && CG < 32) ? lane - g.rowoff * CG : lane;
+  return g;
+}
+
+// 4-pixel group (12 bytes) from 4 packed rgb words
+__device__ __forceinline__ void put_quad(uint32_t* dst, uint32_t p0, uint32_t p1, uint32_t p2,
+                                         uint32_t p3) {
+  dst[0] = __byte_perm(p0, p1, 0x4210);
+  dst[1] = __byte_perm(p1, p2, 0x5421);
+  dst[2] = __byte_perm(p2, p3, 0x6542);
+}
+
+// Render one environment's frame (all 32 lanes of the warp participate).
+// Returns the status of the first failing column (or OK), warp-uniform.
+// _pycore.py:132-271.
+template <int NC>
+__device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
+                          const uint32_t* __restrict__ solid, const WarpSmem& sm, const Env& e, uint8_t* __restrict__ frame,
+                          double* __restrict__ zbuf_out, int32_t* __restrict__ rayinfo,
+                          unsigned long long* __restrict__ spritevis_out, int& bulk_pending,
+                          int& buf, const LaneGeo& lg) {
+  const int lane = threadIdx.x & 31;
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
+  const double planex = -e.dy * PLANE_HALF_WIDTH;
+  const double planey = e.dx * PLANE_HALF_WIDTH;
+
+  // fast march when the rim is sealed and the origin is on the grid
+  const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h;
+  const int st = (S.sealed && inside)
+      ? wall_pass<NC, false>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
+      : wall_pass<NC, true>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo);
+  __syncwarp();
+  if (st != TC_ST_OK) return st;
+  const int m = S.n_ent > 0 ? sprite_setup(S, sm, e, planex, planey, spritevis_out) : 0;
+  if (S.n_ent == 0 && spritevis_out && lane == 0) *spritevis_out = 0;
+
+  if (S.mirror) {
+    // Mirrored bands (even H <= 254, W % 16 == 0). Row r and row H-1-r have
+    // the same wall / non-wall pattern (t0 = h2-half, b0 = h2+half), so one
+    // SWAR compare serves both: per byte, (0x80|r) - t0 has its MSB set iff
+    // r >= t0 (r, t0 <= 127, no inter-byte borrow). PRMT sign-replication
+    // turns the 4 per-pixel flags of a quad into the 3 byte masks of its 12
+    // bytes, and one LOP3 per word blends wall with ceiling (top row) or
+    // floor (bottom row). A lane owns 16 columns (48 bytes = 3 x 16B stores).
+    const int row_bytes = W * 3;
+    const int B = S.band_rows;
+    const int CG = W >> 4;
+    const int RPI = S.mir_rpi;
+    const int rowoff = lg.rowoff;
+    const int cg0 = lg.cg0;
+    const uint32_t C = S.ceil_rgb, F = S.floor_rgb;
+    const uint32_t cw0 = __byte_perm(C, C, 0x4210), cw1 = __byte_perm(C, C, 0x5421),
+                   cw2 = __byte_perm(C, C, 0x6542);
+    const uint32_t fw0 = __byte_perm(F, F, 0x4210), fw1 = __byte_perm(F, F, 0x5421),
+                   fw2 = __byte_perm(F, F, 0x6542);
+    for (int r_lo = 0; r_lo < h2; r_lo += B, buf ^= 1) {
+      const int rows = min(B, h2 - r_lo);
+      uint8_t* top = sm.band[2 * buf];
+      uint8_t* bot = sm.band[2 * buf + 1];
+      const int r_bot = H - r_lo - rows;  // first frame row of the bottom band
+      if (lane == 0 && bulk_pending > 1) bulk_wait_read_le1();
+      __syncwarp();
+      if (rowoff < RPI) {
+        for (int cg = cg0; cg < CG; cg += 32) {
+          const uint4 T = *reinterpret_cast<const uint4*>(sm.t8 + 16 * cg);
+          const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb + 16 * cg);
+          uint32_t Wd[12];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const uint4 w = wp[j];
+            Wd[3 * j + 0] = __byte_perm(w.x, w.y, 0x4210);
+            Wd[3 * j + 1] = __byte_perm(w.y, w.z, 0x5421);
+            Wd[3 * j + 2] = __byte_perm(w.z, w.w, 0x6542);
+          }
+          const uint32_t Tj[4] = {T.x, T.y, T.z, T.w};
+          for (int rr = rowoff; rr < rows; rr += RPI) {
+            const uint32_t R = 0x80808080u + (uint32_t)(r_lo + rr) * 0x01010101u;
+            uint32_t tw[12], bw[12];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              const uint32_t D = R - Tj[j];
+              const uint32_t m0 = prmt_sx(D, 0x9888), m1 = prmt_sx(D, 0xAA99),
+                             m2 = prmt_sx(D, 0xBBBA);
+              tw[3 * j + 0] = (m0 & Wd[3 * j + 0]) | (~m0 & cw0);
+              tw[3 * j + 1] = (m1 & Wd[3 * j + 1]) | (~m1 & cw1);
+              tw[3 * j + 2] = (m2 & Wd[3 * j + 2]) | (~m2 & cw2);
+              bw[3 * j + 0] = (m0 & Wd[3 * j + 0]) | (~m0 & fw0);
+              bw[3 * j + 1] = (m1 & Wd[3 * j + 1]) | (~m1 & fw1);
+              bw[3 * j + 2] = (m2 & Wd[3 * j + 2]) | (~m2 & fw2);
+            }
+            uint4* dt = reinterpret_cast<uint4*>(top + rr * row_bytes + cg * 48);
+            uint4* db = reinterpret_cast<uint4*>(bot + (rows - 1 - rr) * row_bytes + cg * 48);
+            dt[0] = make_uint4(tw[0], tw[1], tw[2], tw[3]);
+            dt[1] = make_uint4(tw[4], tw[5], tw[6], tw[7]);
+            dt[2] = make_uint4(tw[8], tw[9], tw[10], tw[11]);
+            db[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+            db[1] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
+            db[2] = make_uint4(bw[8], bw[9], bw[10], bw[11]);
+          }
+        }
+      }
+      if (m > 0) {
+        __syncwarp();
+        draw_sprites(S, sm, m, top, r_lo, bot, r_bot, rows);
+      }
+      bulk_fence();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_copy(frame + (size_t)r_lo * row_bytes, top, (uint32_t)(rows * row_bytes));
+        bulk_copy(frame + (size_t)r_bot * row_bytes, bot, (uint32_t)(rows * row_bytes));
+        bulk_commit();
+        bulk_pending++;
+      }
+    }
+    __syncwarp();
+    return TC_ST_OK;
   }
 
-  // ---- frame: bands of rows staged in shared memory
+  // Row classes, warp-uniform: [0,tmin) ceiling everywhere, [tmin,tmax)
+  // mixed ceiling/wall, [tmax,bmin) wall everywhere, [bmin,bmax) mixed
+  // wall/floor, [bmax,H) floor everywhere (t0 <= h2 <= b0 per column).
+  int tlo = 0x7fffffff, thi = 0, blo = 0x7fffffff, bhi = 0;
+  for (int c = lane; c < W; c += 32) {
+    const int t = sm.t0[c], b = sm.b0[c];
+    tlo = min(tlo, t); thi = max(thi, t); blo = min(blo, b); bhi = max(bhi, b);
+  }
+  const int tmin = warp_min(tlo), tmax = warp_max(thi);
+  const int bmin = warp_min(blo), bmax = warp_max(bhi);
+
   const int row_bytes = W * 3;
   const int B = S.band_rows;
-  const uint32_t ceil_rgb = S.ceil_rgb, floor_rgb = S.floor_rgb;
+  const uint32_t C = S.ceil_rgb, F = S.floor_rgb;
+  const uint32_t c0w = __byte_perm(C, C, 0x4210), c1w = __byte_perm(C, C, 0x5421),
+                 c2w = __byte_perm(C, C, 0x6542);
+  const uint32_t f0w = __byte_perm(F, F, 0x4210), f1w = __byte_perm(F, F, 0x5421),
+                 f2w = __byte_perm(F, F, 0x6542);
+  const int Q = W >> 2;
+  const int G = Q >= 32 ? 1 : 32 / Q;  // row groups per warp
+  const int rsub = Q >= 32 ? 0 : lane / Q;
+  const int q_first = Q >= 32 ? lane : lane - rsub * Q;
+
   for (int r_lo = 0; r_lo < H; r_lo += B, buf ^= 1) {
     const int rows = min(B, H - r_lo);
+    const int r_end = r_lo + rows;
     uint8_t* band = sm.band[buf];
     // the buffer we are about to overwrite was shipped two bands ago
     if (S.bulk && lane == 0 && bulk_pending > 1) bulk_wait_read_le1();
     __syncwarp();
     if (S.quads) {
-      // 4-pixel groups: 12 bytes = 3 words, packed with PRMT
-      const int Q = W >> 2;
-      const int items = rows * Q;
-      for (int g = lane; g < items; g += 32) {
-        const int rr = g / Q, q = g - rr * Q;
-        const int row = r_lo + rr;
-        const uint2 t4 = *reinterpret_cast<const uint2*>(sm.t0 + 4 * q);
-        const uint2 b4 = *reinterpret_cast<const uint2*>(sm.b0 + 4 * q);
-        const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb + 4 * q);
-        uint32_t px[4];
-        const uint32_t tt[4] = {t4.x & 0xffffu, t4.x >> 16, t4.y & 0xffffu, t4.y >> 16};
-        const uint32_t bb[4] = {b4.x & 0xffffu, b4.x >> 16, b4.y & 0xffffu, b4.y >> 16};
-        const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-          px[k] = (uint32_t)row < tt[k] ? ceil_rgb : ((uint32_t)row < bb[k] ? ww[k] : floor_rgb);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(band + rr * row_bytes + q * 12);
-        dst[0] = __byte_perm(px[0], px[1], 0x4210);
-        dst[1] = __byte_perm(px[1], px[2], 0x5421);
-        dst[2] = __byte_perm(px[2], px[3], 0x6542);
+      if (rsub < G) {
+        for (int q = q_first; q < Q; q += 32) {
+          const uint2 t4 = *reinterpret_cast<const uint2*>(sm.t0 + 4 * q);
+          const uint2 b4 = *reinterpret_cast<const uint2*>(sm.b0 + 4 * q);
+          const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb + 4 * q);
+          const int t0 = t4.x & 0xffff, t1 = t4.x >> 16, t2 = t4.y & 0xffff, t3 = t4.y >> 16;
+          const int b0 = b4.x & 0xffff, b1 = b4.x >> 16, b2 = b4.y & 0xffff, b3 = b4.y >> 16;
+          const uint32_t w0w = __byte_perm(w4.x, w4.y, 0x4210),
+                         w1w = __byte_perm(w4.y, w4.z, 0x5421),
+                         w2w = __byte_perm(w4.z, w4.w, 0x6542);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(band + rsub * row_bytes + q * 12);
+          const int dstep = G * row_bytes / 4;
+          int row = r_lo + rsub;
+          for (const int lim = min(r_end, tmin); row < lim; row += G, dst += dstep) {
+            dst[0] = c0w; dst[1] = c1w; dst[2] = c2w;
+          }
+          for (const int lim = min(r_end, tmax); row < lim; row += G, dst += dstep)
+            put_quad(dst, row < t0 ? C : w4.x, row < t1 ? C : w4.y, row < t2 ? C : w4.z,
+                     row < t3 ? C : w4.w);
+          for (const int lim = min(r_end, bmin); row < lim; row += G, dst += dstep) {
+            dst[0] = w0w; dst[1] = w1w; dst[2] = w2w;
+          }
+          for (const int lim = min(r_end, bmax); row < lim; row += G, dst += dstep)
+            put_quad(dst, row < b0 ? w4.x : F, row < b1 ? w4.y : F, row < b2 ? w4.z : F,
+                     row < b3 ? w4.w : F);
+          for (; row < r_end; row += G, dst += dstep) {
+            dst[0] = f0w; dst[1] = f1w; dst[2] = f2w;
+          }
+        }
       }
     } else {
       const int items = rows * W;
       for (int p = lane; p < items; p += 32) {
         const int rr = p / W, c = p - rr * W;
         const uint32_t row = (uint32_t)(r_lo + rr);
-        const uint32_t col = row < sm.t0[c] ? ceil_rgb : (row < sm.b0[c] ? sm.wrgb[c] : floor_rgb);
+        const uint32_t col = row < sm.t0[c] ? C : (row < sm.b0[c] ? sm.wrgb[c] : F);
         uint8_t* d = band + rr * row_bytes + c * 3;
         d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
       }
     }
-    __syncwarp();
-    // sprites in draw order overwrite their pixels; lane L owns columns
-    // L + 32j (the same lane that holds zbuf for them), _pycore.py:253-270
-    for (int s = 0; s < m; s++) {
-      const SpriteRec& r = sm.recs[s];
-      if (r.denom <= 0) continue;
-      const int ra = max(r.r0, r_lo), rb = min(r.r1, r_lo + rows);
-      if (ra >= rb) continue;
-      double aa[NC], ea[NC];
-      bool vis[NC];
-      bool anyvis = false;
-#pragma unroll
-      for (int j = 0; j < NC; j++) {
-        const int c = lane + 32 * j;
-        vis[j] = false;
-        aa[j] = 0.0;
-        ea[j] = 0.0;
-        if (c < W && !(zb[j] <= r.dep)) {
-          const double a = (S.coef[c] - r.ks) / r.halfk;
-          if (!(a <= -1.0 || a >= 1.0)) {
-            vis[j] = true;
-            aa[j] = a >= 0.0 ? a : -a;
-            if (r.kd == K_KEY) ea[j] = aa[j] / 0.30;
-          }
-        }
-        anyvis |= vis[j];
-      }
-      if (!__any_sync(0xffffffffu, anyvis)) continue;
-      const double denom = (double)r.denom;
-      for (int row = ra; row < rb; row++) {
-        const double v = ((double)(row - r.vtop) + 0.5) / denom;
-        const double ev = r.kd == K_KEY ? (v - 0.30) / 0.18 : 0.0;
-        uint8_t* drow = band + (row - r_lo) * row_bytes;
-#pragma unroll
-        for (int j = 0; j < NC; j++) {
-          if (!vis[j]) continue;
-          const int mk = sprite_mask(r.kd, aa[j], ea[j], v, ev);
-          if (mk) {
-            const uint32_t col = mk == 1 ? r.s1 : r.s2;
-            uint8_t* d = drow + (lane + 32 * j) * 3;
-            d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
-          }
-        }
-      }
+    if (m > 0) {
+      __syncwarp();
+      draw_sprites(S, sm, m, band, r_lo, nullptr, 0, rows);
     }
     // ship the band
     const int bytes = rows * row_bytes;
@@ -790,34 +1074,54 @@ __device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, 
     st.ealive[i * S.n_ent + lane + 32] = (uint8_t)((e.emask >> (lane + 32)) & 1ULL);
 }
 
-__device__ __forceinline__ const uint32_t* stage_map(const SpecDev& S, uint32_t* smap) {
-  if (!S.smem_map) return S.cell;
+// packed cells + stop codes into shared memory once per CTA
+__device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, const uint32_t*& cell,
+                                          const uint32_t*& solid) {
+  if (!S.smem_map) {
+    cell = S.cell;
+    solid = S.solid;
+    return;
+  }
   const int cells = S.h * S.w;
-  for (int k = threadIdx.x; k < cells; k += blockDim.x) smap[k] = S.cell[k];
+  for (int k = threadIdx.x; k < cells; k += blockDim.x) {
+    smap[k] = S.cell[k];
+    smap[cells + k] = S.solid[k];
+  }
   __syncthreads();
-  return smap;
+  cell = smap;
+  solid = smap + cells;
 }
+
 
 // MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387
 template <int NC>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
 batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutDev out,
              long long n, int mode, int auto_reset, int validate,
              tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
-  const int map_bytes = S.smem_map ? align16(S.h * S.w * 4) : 0;
-  const uint32_t* cell = stage_map(S, smap);
+  const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
+  const uint32_t *cell, *solid;
+  stage_map(S, smap, cell, solid);
   const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
                             S.band_stride);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
+  const LaneGeo lg = lane_geo(S);
   int bulk_pending = 0, buf = 0;
   unsigned long long viol = 0;
   uint32_t badbits = 0;
-
-  for (long long i = (long long)blockIdx.x * WARPS_PER_CTA + warp; i < n;
-       i += (long long)gridDim.x * WARPS_PER_CTA) {
+  // env scheduling: env i0 = global warp id first; envs beyond one wave are
+  // pulled dynamically from a device ticket counter (self-resetting: the
+  // last CTA to finish zeroes it for the next launch)
+  const long long stride = (long long)gridDim.x * WARPS_PER_CTA;
+  const bool dyn = counters != nullptr && n > stride;
+  long long i = (long long)blockIdx.x * WARPS_PER_CTA + warp;
+  while (i < n) {
+    // grab the next ticket now; its latency hides behind this env's work
+    long long tnext = i + stride;
+    if (dyn && lane == 0) tnext = stride + (long long)atomicAdd(&counters->next_env, 1u);
     Env e;
     int status = TC_ST_OK;
     if (mode == MODE_RESET) {
@@ -832,7 +1136,7 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
         if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
           status = TC_ST_BAD_ACTION;
         } else {
-          const StepOut o = step_dynamics(S, cell, e, (int)act, validate);
+          const StepOut o = step_dynamics(S, cell, solid, e, (int)act, validate);
           if (lane == 0) {
             out.rewards[i] = o.reward;
             out.dones[i] = (uint8_t)o.done;
@@ -846,13 +1150,14 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
       }
     }
     if (status == TC_ST_OK) {
-      status = render_env<NC>(S, cell, sm, e, out.frames + (size_t)i * frame_bytes,
+      status = render_env<NC>(S, cell, solid, sm, e, out.frames + (size_t)i * frame_bytes,
                               out.zbuf ? out.zbuf + (size_t)i * S.obs_w : nullptr,
                               out.rayinfo ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
-                              out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf);
+                              out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf, lg);
     }
     if (lane == 0) out.statuses[i] = status;
     if (status != TC_ST_OK) badbits |= 1u << status;
+    i = dyn ? __shfl_sync(0xffffffffu, tnext, 0) : i + stride;
   }
   if (lane == 0) {
     if (bulk_pending) bulk_wait_all();
@@ -861,22 +1166,34 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
       if (badbits) atomicOr(&counters->bad_status, badbits);
     }
   }
+  if (dyn) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&counters->ctas_done, 1u) == gridDim.x - 1) {
+        counters->next_env = 0;
+        counters->ctas_done = 0;
+      }
+    }
+  }
 }
 
 // K fused steps with on-device policy actions (batch.py:141-153 draws) and
 // auto-reset; the env's state stays in registers across steps.
 template <int NC>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32)
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
 rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
                tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
-  const int map_bytes = S.smem_map ? align16(S.h * S.w * 4) : 0;
-  const uint32_t* cell = stage_map(S, smap);
+  const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
+  const uint32_t *cell, *solid;
+  stage_map(S, smap, cell, solid);
   const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
                             S.band_stride);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
+  const LaneGeo lg = lane_geo(S);
   int bulk_pending = 0, buf = 0;
   uint32_t badbits = 0;
 
@@ -885,11 +1202,12 @@ rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
     Env e;
     int st_acc = TC_ST_OK;
     load_env(S, st, i, e);
+    int ring_k = 0;
     for (int k = 0; k < ra.k_steps; k++) {
       const long long step = ra.step0 + k;
       unsigned long long ctr = (unsigned long long)(step * ra.n_total + ra.base + i);
       const int act = ra.tags[draw_below(ra.policy_key, ctr, (uint64_t)ra.n_tags)];
-      const StepOut o = step_dynamics(S, cell, e, act, 0);
+      const StepOut o = step_dynamics(S, cell, solid, e, act, 0);
       const size_t kn = (size_t)k * (size_t)n + (size_t)i;
       if (lane == 0) {
         if (out.rewards) out.rewards[kn] = o.reward;
@@ -898,9 +1216,10 @@ rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
         if (out.events) out.events[kn] = o.events;
       }
       if (o.done) reset_draws(S, e);
-      const size_t slot = (size_t)(k % ra.frame_ring) * (size_t)n + (size_t)i;
-      const int status = render_env<NC>(S, cell, sm, e, out.frames + slot * frame_bytes,
-                                        nullptr, nullptr, nullptr, bulk_pending, buf);
+      const size_t slot = (size_t)ring_k * (size_t)n + (size_t)i;
+      if (++ring_k == ra.frame_ring) ring_k = 0;
+      const int status = render_env<NC>(S, cell, solid, sm, e, out.frames + slot * frame_bytes,
+                                        nullptr, nullptr, nullptr, bulk_pending, buf, lg);
       if (status != TC_ST_OK) {
         badbits |= 1u << status;
         if (st_acc == TC_ST_OK) st_acc = status;
@@ -1010,7 +1329,8 @@ const void* select_rollout(int nc) {
 }
 
 // validates host tables and builds the packed cell words
-int validate_tables(const tc_tables* t, std::vector<uint32_t>& cells) {
+int validate_tables(const tc_tables* t, std::vector<uint32_t>& cells,
+                    std::vector<uint32_t>& solid, int& sealed) {
   if (!t) return fail(TC_E_INVALID, "tables is NULL");
   if (t->h < 1 || t->w < 1) return fail(TC_E_INVALID, "empty map");
   if (t->obs_w < 8 || t->obs_h < 8) return fail(TC_E_INVALID, "observation must be at least 8x8");
@@ -1023,6 +1343,7 @@ int validate_tables(const tc_tables* t, std::vector<uint32_t>& cells) {
   if (t->n_pal < 1 || t->n_pal > 256) return fail(TC_E_INVALID, "palette size must be 1..256");
   const int cells_n = t->h * t->w;
   cells.assign(cells_n, 0);
+  solid.assign(cells_n, 0);
   for (int k = 0; k < cells_n; k++) {
     const uint32_t tag = t->kind[k];
     uint32_t idx = 0;
@@ -1043,7 +1364,13 @@ int validate_tables(const tc_tables* t, std::vector<uint32_t>& cells) {
       eat = (uint32_t)ei + 1;
     }
     cells[k] = idx | (tag << CELL_TAG_SHIFT) | (eat << CELL_EAT_SHIFT);
+    solid[k] = tag == C_WALL ? 0xffffffffu : tag == C_DOOR ? (1u << idx) : 0u;
   }
+  sealed = 1;
+  for (int y = 0; y < t->h; y++)
+    for (int x = 0; x < t->w; x++)
+      if ((y == 0 || y == t->h - 1 || x == 0 || x == t->w - 1) && t->kind[y * t->w + x] != C_WALL)
+        sealed = 0;
   for (int d = 0; d < t->n_doors; d++)
     if (t->dcol[d] > 2) return fail(TC_E_INVALID, "door colour must be 0..2");
   for (int e = 0; e < t->n_entities; e++) {
@@ -1083,14 +1410,16 @@ int launch_geometry(tc_spec* s) {
   const int row_bytes = d.obs_w * 3;
   d.quads = (d.obs_w % 4) == 0;
   d.bulk = (row_bytes % 16) == 0;
-  int rows = BAND_BYTES_TARGET / row_bytes;
+  d.mirror = (d.obs_h % 2 == 0 && d.obs_h <= 254 && d.obs_w % 16 == 0 && d.bulk) ? 1 : 0;
+  d.mir_rpi = (d.obs_w / 16) >= 32 ? 1 : 32 / (d.obs_w / 16 > 0 ? d.obs_w / 16 : 1);
+  int rows = (d.mirror ? BAND_BYTES_TARGET / 2 : BAND_BYTES_TARGET) / row_bytes;
   if (rows < 1) rows = 1;
   if (rows > d.obs_h) rows = d.obs_h;
   d.band_rows = rows;
   d.band_stride = align16(rows * row_bytes);
   d.warp_smem = align16(warp_smem_bytes(d.obs_w, d.n_ent, d.band_stride));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
-  const size_t map_bytes = d.smem_map ? (size_t)align16(d.h * d.w * 4) : 0;
+  const size_t map_bytes = d.smem_map ? (size_t)align16(d.h * d.w * 8) : 0;
   s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * d.warp_smem;
   s->nc = pick_nc(d.obs_w);
   const void* fns[2] = {select_batch(s->nc), select_rollout(s->nc)};
@@ -1150,8 +1479,9 @@ const char* tc_build_info(void) {
 int tc_spec_create(const tc_tables* t, tc_spec** out) {
   if (!out) return fail(TC_E_INVALID, "out is NULL");
   *out = nullptr;
-  std::vector<uint32_t> cells;
-  int rc = validate_tables(t, cells);
+  std::vector<uint32_t> cells, solid;
+  int sealed = 0;
+  int rc = validate_tables(t, cells, solid, sealed);
   if (rc != TC_OK) return rc;
 
   std::vector<uint32_t> pal(t->n_pal), doorrgb(t->n_doors);
@@ -1160,6 +1490,7 @@ int tc_spec_create(const tc_tables* t, tc_spec** out) {
 
   BlobBuilder b;
   const size_t o_cell = b.add(cells.data(), cells.size() * 4);
+  const size_t o_solid = b.add(solid.data(), solid.size() * 4);
   const size_t o_pal = b.add(pal.data(), pal.size() * 4);
   const size_t o_door = b.add(doorrgb.data(), doorrgb.size() * 4);
   const size_t o_dcol = b.add(t->dcol, t->n_doors);
@@ -1181,6 +1512,8 @@ int tc_spec_create(const tc_tables* t, tc_spec** out) {
   uint8_t* base = static_cast<uint8_t*>(s->blob);
   SpecDev& d = s->dev;
   d.cell = (const uint32_t*)(base + o_cell);
+  d.solid = (const uint32_t*)(base + o_solid);
+  d.sealed = sealed;
   d.pal = (const uint32_t*)(base + o_pal);
   d.doorrgb = (const uint32_t*)(base + o_door);
   d.dcol = base + o_dcol;

@@ -161,8 +161,8 @@ class DeviceOut:
 
 
 def new_counters(device) -> torch.Tensor:
-    """tc_counters (16 bytes) accumulated on device, read lazily."""
-    return torch.zeros(2, dtype=torch.int64, device=device)
+    """tc_counters (24 bytes, zeroed) accumulated on device, read lazily."""
+    return torch.zeros(3, dtype=torch.int64, device=device)
 
 
 def read_counters(c: torch.Tensor) -> tuple[int, int]:
