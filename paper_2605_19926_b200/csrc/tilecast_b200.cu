@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -56,6 +57,12 @@ constexpr uint64_t MIX2 = 0x94D049BB133111EBULL;
 constexpr uint64_t SPLIT_SALT = 0x3C6EF372FE94F82AULL;
 
 constexpr int WARPS_PER_CTA = 4;
+#ifndef TC_EXPERIMENT
+#define TC_EXPERIMENT 0  // perf experiments only: 1 = skip sprites, 2 = skip sprite draw
+#endif
+#ifndef TC_TRACE
+#define TC_TRACE 0  // perf experiments only: per-env phase timestamps
+#endif
 #ifndef TC_MIN_CTAS
 #define TC_MIN_CTAS 5  // resident CTAs per SM the register budget is sized for
 #endif
@@ -152,6 +159,21 @@ struct SpriteRec {
   uint32_t s1, s2;  // shaded main / secondary colour
   int kd, ent;
 };
+
+#if TC_TRACE
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(i, slot)                                                   \
+  do {                                                                   \
+    if (g_trace && (threadIdx.x & 31) == 0) g_trace[(i) * 8 + (slot)] = gtime(); \
+  } while (0)
+#else
+#define TRACE(i, slot) do { } while (0)
+#endif
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -685,6 +707,10 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         lat = invdet * (e.dy * relx - e.dx * rely);
         dep = invdet * (-planey * relx + planex * rely);
         keep = !(dep < S.fc[FC_MIN_SPRITE_DEPTH]);
+        // conservative horizontal-FOV cull (no division): if |lat| exceeds
+        // (dep + K)(1 + 1e-6) then |ks| > 1 + halfk by a margin far above
+        // rounding, so every column's |a| >= 1 and the sprite draws nothing
+        if (keep && fabs(lat) > (dep + S.fc[FC_SPRITE_K]) * (1.0 + 1e-6)) keep = false;
       }
       uint32_t bal = __ballot_sync(0xffffffffu, keep);
       while (bal) {  // warp-uniform walk over the gathered sprites
@@ -692,14 +718,20 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         bal &= bal - 1u;
         const double d = __shfl_sync(0xffffffffu, dep, src);
         const double l = __shfl_sync(0xffffffffu, lat, src);
-        double sh_f = (double)H / d;
+        // the four per-sprite quotients, one per lane (same operands and
+        // order as _pycore.py:220-223), then broadcast
+        const double qn = lane == 0 ? (double)H : lane == 1 ? l : lane == 2 ? spk : 1.0;
+        const double qd = lane == 3 ? 1.0 + atten * d : d;
+        const double q = qn / qd;
+        double sh_f = __shfl_sync(0xffffffffu, q, 0);
+        const double ks = __shfl_sync(0xffffffffu, q, 1);
+        const double halfk = __shfl_sync(0xffffffffu, q, 2);
+        const double shade = __shfl_sync(0xffffffffu, q, 3);
         if (sh_f > 1e9) sh_f = 1e9;
         const int vhalf = (int)sh_f / 2;
         const int vtop = h2 - vhalf, vbot = h2 + vhalf;
         const int r0 = vtop > 0 ? vtop : 0, r1 = vbot < H ? vbot : H;
         if (vbot - vtop <= 0 || r0 >= r1) continue;
-        const double ks = l / d;
-        const double halfk = spk / d;
         bool any = false;
         for (int c = lane; c < W; c += 32) {
           if (!(sm.zbuf[c] <= d)) {
@@ -720,7 +752,6 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
           r.r1 = r1;
           r.kd = S.ekind[en];
           r.ent = en;
-          const double shade = 1.0 / (1.0 + atten * d);
           const uint32_t m1 = r.kd == K_KEY ? S.key_rgb[S.ecol[en]]
                               : r.kd == K_GOAL ? S.goal_rgb : S.med_cross;
           r.s1 = rgb_scale(m1, shade);
@@ -769,45 +800,69 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
 
 // Sprites in draw order overwrite their pixels of the staged band(s); lane
 // L owns columns L + 32j (_pycore.py:253-270). bandB (may be NULL) is a
-// second band of the same height (the mirrored bottom band). Per-column
-// terms (a, |a|, key ellipse x) and per-row terms (v, key ellipse y) are
-// computed once per band; the mask comparisons are the reference's.
+// second band of the same height (the mirrored bottom band). Per column the
+// lane computes a = (coef - ks) / halfk (and the key's aa / 0.30) once per
+// band; per row, v = ((row - vtop) + 0.5) / denom (and the key's
+// (v - 0.30) / 0.18) is computed lane-parallel -- lane k divides for row
+// ra + k -- and broadcast with shuffles. Same doubles, same comparisons as
+// the reference, ~1 division per 32 rows instead of 1 per row.
+template <int NC>
 __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& sm, int m,
-                                          uint8_t* bandA, int rA, uint8_t* bandB, int rB,
-                                          int rows) {
+                                             uint8_t* bandA, int rA, uint8_t* bandB, int rB,
+                                             int rows) {
   const int lane = threadIdx.x & 31;
   const int W = S.obs_w, row_bytes = W * 3;
   for (int s = 0; s < m; s++) {
     const SpriteRec r = sm.recs[s];
     const double denom = (double)r.denom;
+    const bool key = r.kd == K_KEY;
     for (int half = 0; half < 2; half++) {
       uint8_t* band = half ? bandB : bandA;
       const int r_lo = half ? rB : rA;
       if (band == nullptr) continue;
       const int ra = max(r.r0, r_lo), rb = min(r.r1, r_lo + rows);
       if (ra >= rb) continue;
-      for (int c0 = 0; c0 < W; c0 += 32) {
-        const int c = c0 + lane;
-        bool vis = false;
-        double aa = 0.0, ea = 0.0;
+      double aa[NC], ea[NC];
+      bool vis[NC];
+      bool anyv = false;
+#pragma unroll
+      for (int j = 0; j < NC; j++) {
+        const int c = lane + 32 * j;
+        vis[j] = false;
+        aa[j] = 0.0;
+        ea[j] = 0.0;
         if (c < W && !(sm.zbuf[c] <= r.dep)) {
           const double a = (S.coef[c] - r.ks) / r.halfk;
           if (!(a <= -1.0 || a >= 1.0)) {
-            vis = true;
-            aa = a >= 0.0 ? a : -a;
-            if (r.kd == K_KEY) ea = aa / 0.30;
+            vis[j] = true;
+            aa[j] = a >= 0.0 ? a : -a;
+            if (key) ea[j] = aa[j] / 0.30;
           }
         }
-        if (!__any_sync(0xffffffffu, vis)) continue;
-        for (int row = ra; row < rb; row++) {
-          const double v = ((double)(row - r.vtop) + 0.5) / denom;
-          const double ev = r.kd == K_KEY ? (v - 0.30) / 0.18 : 0.0;
-          if (!vis) continue;
-          const int mk = sprite_mask(r.kd, aa, ea, v, ev);
-          if (mk) {
-            const uint32_t col = mk == 1 ? r.s1 : r.s2;
-            uint8_t* d = band + (row - r_lo) * row_bytes + c * 3;
-            d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
+        anyv |= vis[j];
+      }
+      if (!__any_sync(0xffffffffu, anyv)) continue;
+      for (int r32 = ra; r32 < rb; r32 += 32) {
+        // lane-parallel row terms for rows r32 .. r32+31
+        double v_l = 0.0, ev_l = 0.0;
+        if (r32 + lane < rb) {
+          v_l = ((double)(r32 + lane - r.vtop) + 0.5) / denom;
+          if (key) ev_l = (v_l - 0.30) / 0.18;
+        }
+        const int nr = min(32, rb - r32);
+        for (int k = 0; k < nr; k++) {
+          const double v = __shfl_sync(0xffffffffu, v_l, k);
+          const double ev = __shfl_sync(0xffffffffu, ev_l, k);
+          uint8_t* drow = band + (r32 + k - r_lo) * row_bytes;
+#pragma unroll
+          for (int j = 0; j < NC; j++) {
+            if (!vis[j]) continue;
+            const int mk = sprite_mask(r.kd, aa[j], ea[j], v, ev);
+            if (mk) {
+              const uint32_t col = mk == 1 ? r.s1 : r.s2;
+              uint8_t* d = drow + (lane + 32 * j) * 3;
+              d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
+            }
           }
         }
       }
@@ -839,28 +894,44 @@ __device__ __forceinline__ void put_quad(uint32_t* dst, uint32_t p0, uint32_t p1
 // Render one environment's frame (all 32 lanes of the warp participate).
 // Returns the status of the first failing column (or OK), warp-uniform.
 // _pycore.py:132-271.
+// Phase 1 of rendering: wall pass (spans / zbuf into shared memory).
 template <int NC>
-__device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
-                          const uint32_t* __restrict__ solid, const WarpSmem& sm, const Env& e, uint8_t* __restrict__ frame,
-                          double* __restrict__ zbuf_out, int32_t* __restrict__ rayinfo,
-                          unsigned long long* __restrict__ spritevis_out, int& bulk_pending,
-                          int& buf, const LaneGeo& lg) {
-  const int lane = threadIdx.x & 31;
-  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
+__device__ __forceinline__ int render_walls(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                            const uint32_t* __restrict__ solid,
+                                            const WarpSmem& sm, const Env& e,
+                                            double* __restrict__ zbuf_out,
+                                            int32_t* __restrict__ rayinfo) {
   const double planex = -e.dy * PLANE_HALF_WIDTH;
   const double planey = e.dx * PLANE_HALF_WIDTH;
-
   // fast march when the rim is sealed and the origin is on the grid
   const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h;
   const int st = (S.sealed && inside)
       ? wall_pass<NC, false>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
       : wall_pass<NC, true>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo);
   __syncwarp();
-  if (st != TC_ST_OK) return st;
-  const int m = S.n_ent > 0 ? sprite_setup(S, sm, e, planex, planey, spritevis_out) : 0;
-  if (S.n_ent == 0 && spritevis_out && lane == 0) *spritevis_out = 0;
+  return st;
+}
 
-  if (S.mirror) {
+// Phase 2: sprite setup; returns the number of sprites that draw.
+__device__ __forceinline__ int render_sprites(const SpecDev& S, const WarpSmem& sm, const Env& e,
+                                              unsigned long long* __restrict__ spritevis_out) {
+  if (S.n_ent == 0 || TC_EXPERIMENT == 1) {
+    if (spritevis_out && (threadIdx.x & 31) == 0) *spritevis_out = 0;
+    return 0;
+  }
+  const double planex = -e.dy * PLANE_HALF_WIDTH;
+  const double planey = e.dx * PLANE_HALF_WIDTH;
+  const int m = sprite_setup(S, sm, e, planex, planey, spritevis_out);
+  return TC_EXPERIMENT == 2 ? 0 : m;
+}
+
+// Mirrored-band compose + sprites + TMA store (see render_frame_out).
+template <int NC, bool SPR>
+__device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& sm, int m,
+                                             uint8_t* __restrict__ frame, int& bulk_pending,
+                                             int& buf, const LaneGeo& lg) {
+  const int lane = threadIdx.x & 31;
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
     // Mirrored bands (even H <= 254, W % 16 == 0). Row r and row H-1-r have
     // the same wall / non-wall pattern (t0 = h2-half, b0 = h2+half), so one
     // SWAR compare serves both: per byte, (0x80|r) - t0 has its MSB set iff
@@ -925,9 +996,9 @@ __device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
           }
         }
       }
-      if (m > 0) {
+      if (SPR && m > 0) {
         __syncwarp();
-        draw_sprites(S, sm, m, top, r_lo, bot, r_bot, rows);
+        draw_sprites<NC>(S, sm, m, top, r_lo, bot, r_bot, rows);
       }
       bulk_fence();
       __syncwarp();
@@ -938,8 +1009,19 @@ __device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
         bulk_pending++;
       }
     }
-    __syncwarp();
-    return TC_ST_OK;
+  __syncwarp();
+}
+
+// Phase 3: compose the frame in staged bands, draw sprites, ship with TMA.
+template <int NC>
+__device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSmem& sm, int m,
+                                                 uint8_t* __restrict__ frame, int& bulk_pending,
+                                                 int& buf, const LaneGeo& lg) {
+  const int lane = threadIdx.x & 31;
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
+  if (S.mirror) {
+    mirror_bands<NC, true>(S, sm, m, frame, bulk_pending, buf, lg);
+    return;
   }
 
   // Row classes, warp-uniform: [0,tmin) ceiling everywhere, [tmin,tmax)
@@ -1015,7 +1097,7 @@ __device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
     }
     if (m > 0) {
       __syncwarp();
-      draw_sprites(S, sm, m, band, r_lo, nullptr, 0, rows);
+      draw_sprites<NC>(S, sm, m, band, r_lo, nullptr, 0, rows);
     }
     // ship the band
     const int bytes = rows * row_bytes;
@@ -1033,10 +1115,31 @@ __device__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
     }
   }
   __syncwarp();
+}
+
+// Render one environment's frame (all 32 lanes of the warp participate).
+// Returns the status of the first failing column (or OK), warp-uniform.
+// _pycore.py:132-271.
+template <int NC>
+__device__ __forceinline__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                          const uint32_t* __restrict__ solid, const WarpSmem& sm,
+                                          const Env& e, uint8_t* __restrict__ frame,
+                                          double* __restrict__ zbuf_out,
+                                          int32_t* __restrict__ rayinfo,
+                                          unsigned long long* __restrict__ spritevis_out,
+                                          int& bulk_pending, int& buf, const LaneGeo& lg,
+                                          long long ti = 0) {
+  const int st = render_walls<NC>(S, cell, solid, sm, e, zbuf_out, rayinfo);
+  if (st != TC_ST_OK) return st;
+  TRACE(ti, 3);
+  const int m = render_sprites(S, sm, e, spritevis_out);
+  TRACE(ti, 4);
+  render_frame_out<NC>(S, sm, m, frame, bulk_pending, buf, lg);
   return TC_ST_OK;
 }
 
 // ------------------------------------------------------------- the kernels
+
 __device__ __forceinline__ void load_env(const SpecDev& S, const StateDev& st, long long i,
                                          Env& e) {
   const int lane = threadIdx.x & 31;
@@ -1124,6 +1227,7 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
     if (dyn && lane == 0) tnext = stride + (long long)atomicAdd(&counters->next_env, 1u);
     Env e;
     int status = TC_ST_OK;
+    TRACE(i, 0);
     if (mode == MODE_RESET) {
       e.rkey = st.rkey[i];
       e.rctr = st.rctr[i];
@@ -1133,6 +1237,7 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
       load_env(S, st, i, e);
       if (mode == MODE_STEP) {
         const long long act = actions[i];
+        TRACE(i, 1);
         if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
           status = TC_ST_BAD_ACTION;
         } else {
@@ -1146,6 +1251,7 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
           viol += (unsigned long long)o.violation;
           if (o.done && auto_reset) reset_draws(S, e);
           store_env(S, st, i, e);
+          TRACE(i, 2);
         }
       }
     }
@@ -1153,10 +1259,19 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
       status = render_env<NC>(S, cell, solid, sm, e, out.frames + (size_t)i * frame_bytes,
                               out.zbuf ? out.zbuf + (size_t)i * S.obs_w : nullptr,
                               out.rayinfo ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
-                              out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf, lg);
+                              out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf, lg, i);
     }
     if (lane == 0) out.statuses[i] = status;
     if (status != TC_ST_OK) badbits |= 1u << status;
+#if TC_TRACE
+    if (g_trace && lane == 0) {
+      unsigned int smid;
+      asm("mov.u32 %0, %smid;" : "=r"(smid));
+      g_trace[i * 8 + 5] = gtime();
+      g_trace[i * 8 + 6] = smid | ((unsigned long long)warp << 16) |
+                           ((unsigned long long)blockIdx.x << 32);
+    }
+#endif
     i = dyn ? __shfl_sync(0xffffffffu, tnext, 0) : i + stride;
   }
   if (lane == 0) {
@@ -1234,6 +1349,76 @@ rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
   }
 }
 
+// Phase-synchronised rollout: the CTA's warps run each step's phases
+// (dynamics | walls | sprites | frame) in lockstep with CTA barriers, so at
+// any moment the SM executes one phase's code (the fused step's full code
+// footprint exceeds the instruction cache; one phase's does not).
+template <int NC, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 3 : 1))
+rollout_phased_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
+                      tc_counters* __restrict__ counters) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
+  const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
+  const uint32_t *cell, *solid;
+  stage_map(S, smap, cell, solid);
+  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
+                            S.band_stride);
+  const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
+  const LaneGeo lg = lane_geo(S);
+  int bulk_pending = 0, buf = 0;
+  uint32_t badbits = 0;
+  for (long long base = (long long)blockIdx.x * WARPS; base < n;
+       base += (long long)gridDim.x * WARPS) {
+    const long long i = base + warp;
+    const bool active = i < n;
+    Env e;
+    int st_acc = TC_ST_OK;
+    if (active) load_env(S, st, i, e);
+    int ring_k = 0;
+    for (int k = 0; k < ra.k_steps; k++) {
+      int status = TC_ST_OK, m = 0;
+      size_t slot = 0;
+      if (active) {
+        const long long step = ra.step0 + k;
+        unsigned long long ctr = (unsigned long long)(step * ra.n_total + ra.base + i);
+        const int act = ra.tags[draw_below(ra.policy_key, ctr, (uint64_t)ra.n_tags)];
+        const StepOut o = step_dynamics(S, cell, solid, e, act, 0);
+        const size_t kn = (size_t)k * (size_t)n + (size_t)i;
+        if (lane == 0) {
+          if (out.rewards) out.rewards[kn] = o.reward;
+          if (out.dones) out.dones[kn] = (uint8_t)o.done;
+          if (out.truncs) out.truncs[kn] = (uint8_t)o.trunc;
+          if (out.events) out.events[kn] = o.events;
+        }
+        if (o.done) reset_draws(S, e);
+        slot = (size_t)ring_k * (size_t)n + (size_t)i;
+      }
+      if (++ring_k == ra.frame_ring) ring_k = 0;
+      __syncthreads();
+      if (active) status = render_walls<NC>(S, cell, solid, sm, e, nullptr, nullptr);
+      __syncthreads();
+      if (active && status == TC_ST_OK) m = render_sprites(S, sm, e, nullptr);
+      __syncthreads();
+      if (active && status == TC_ST_OK)
+        render_frame_out<NC>(S, sm, m, out.frames + slot * frame_bytes, bulk_pending, buf, lg);
+      if (status != TC_ST_OK) {
+        badbits |= 1u << status;
+        if (st_acc == TC_ST_OK) st_acc = status;
+      }
+    }
+    if (active) {
+      store_env(S, st, i, e);
+      if (lane == 0 && out.statuses) out.statuses[i] = st_acc;
+    }
+  }
+  if (lane == 0) {
+    if (bulk_pending) bulk_wait_all();
+    if (counters && badbits) atomicOr(&counters->bad_status, badbits);
+  }
+}
+
 __global__ void seed_kernel(uint64_t root, long long base, long long n,
                             unsigned long long* rkey, unsigned long long* rctr) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -1266,6 +1451,9 @@ __global__ void cast_ray_kernel(const uint32_t* cell, int h, int w, uint32_t dma
 // =================================================================== host
 struct tc_spec {
   SpecDev dev;
+  int phased = 0;        // TILECAST_PHASED=<warps>: phase-synchronised rollout
+  int phased_ctas = 0;
+  size_t phased_smem = 0;
   void* blob = nullptr;
   int nc = 1;
   int max_ctas = 0;  // grid size for one full wave
@@ -1315,6 +1503,27 @@ const void* select_batch(int nc) {
     case 16: return batch_fn<16>();
     default: return batch_fn<32>();
   }
+}
+template <int NC, int WP>
+const void* phased_fn() { return (const void*)rollout_phased_kernel<NC, WP>; }
+const void* select_phased(int nc, int wp) {
+  if (wp == 8) {
+    switch (nc) {
+      case 1: return phased_fn<1, 8>();
+      case 2: return phased_fn<2, 8>();
+      case 4: return phased_fn<4, 8>();
+      default: return nullptr;
+    }
+  }
+  if (wp == 16) {
+    switch (nc) {
+      case 1: return phased_fn<1, 16>();
+      case 2: return phased_fn<2, 16>();
+      case 4: return phased_fn<4, 16>();
+      default: return nullptr;
+    }
+  }
+  return nullptr;
 }
 const void* select_rollout(int nc) {
   switch (nc) {
@@ -1438,6 +1647,20 @@ int launch_geometry(tc_spec* s) {
                                                         s->smem_bytes));
   if (per_sm < 1) return fail(TC_E_CAPACITY, "kernel does not fit on an SM");
   s->max_ctas = per_sm * device_sm_count();
+  const char* ph = getenv("TILECAST_PHASED");
+  s->phased = ph ? atoi(ph) : 0;
+  if (s->phased && select_phased(s->nc, s->phased)) {
+    const void* fn = select_phased(s->nc, s->phased);
+    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    s->phased_smem = map_bytes + (size_t)s->phased * d.warp_smem;
+    int pc = 0;
+    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pc, fn, s->phased * 32,
+                                                          s->phased_smem));
+    s->phased_ctas = pc * device_sm_count();
+    if (pc < 1) s->phased = 0;
+  } else {
+    s->phased = 0;
+  }
   return TC_OK;
 }
 
@@ -1471,6 +1694,17 @@ int grid_for(const tc_spec* s, int64_t n) {
 extern "C" {
 
 int tc_abi_version(void) { return TC_ABI_VERSION; }
+
+// perf-experiment hook: per-env phase timestamps (TC_TRACE builds only)
+int tc_debug_trace(void* dev_buf) {
+#if TC_TRACE
+  TC_CUDA(cudaMemcpyToSymbol(g_trace, &dev_buf, sizeof(void*)));
+  return TC_OK;
+#else
+  (void)dev_buf;
+  return fail(TC_E_INVALID, "library built without TC_TRACE");
+#endif
+}
 const char* tc_last_error(void) { return g_err.c_str(); }
 const char* tc_build_info(void) {
   return "tilecast_b200 sm_100a; fp64 --fmad=false; warps/cta=4; TMA bulk-store bands";
@@ -1609,10 +1843,17 @@ int tc_rollout(const tc_spec* s, const tc_state* state, const tc_out* out, int64
   if (ra.n_tags == 0) return fail(TC_E_INVALID, "spec has no legal actions");
   StateDev sd = to_dev(state);
   OutDev od = to_dev(out);
-  const int grid = grid_for(s, n);
   const long long nn = n;
   SpecDev spec = s->dev;
   void* args[] = {&spec, &sd, &od, (void*)&nn, &ra, &counters_dev};
+  if (s->phased) {
+    const int64_t want = (n + s->phased - 1) / s->phased;
+    const int g = (int)(want < s->phased_ctas ? want : s->phased_ctas);
+    TC_CUDA(cudaLaunchKernel(select_phased(s->nc, s->phased), dim3(g), dim3(s->phased * 32),
+                             args, s->phased_smem, (cudaStream_t)stream));
+    return TC_OK;
+  }
+  const int grid = grid_for(s, n);
   TC_CUDA(cudaLaunchKernel(select_rollout(s->nc), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
                            s->smem_bytes, (cudaStream_t)stream));
   return TC_OK;
