@@ -267,11 +267,16 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_2605_19926_b200.shard import reduce_episode_stats, shard_range
+
     spec = make_spec(args.config)
-    n = CONFIGS[args.config][2]
-    if args.config == "c5":
-        n = (1 << 20) // max(world, 1) if world > 1 else CONFIGS["c5"][2]
-    base, n_total = rank * n, world * n
+    # c2-c4: fixed envs per GPU (weak scaling); c5: 2^20 envs in total split
+    # over the GPUs (strong scaling) -- 131072 on one GPU keeps it in minutes
+    n_cfg = CONFIGS[args.config][2]
+    n_total = (1 << 20) if (args.config == "c5" and world > 1) else n_cfg * world
+    sh = shard_range(n_total, world, rank)
+    n, base = sh.n, sh.base
+    scaling = "strong" if (args.config == "c5" and world > 1) else "weak"
     H, W = spec.obs_height, spec.obs_width
     frame_bytes = n * H * W * 3
     ring = max(2, -(-2 * L2_BYTES // frame_bytes))  # >= 2x L2 of frame blocks
@@ -360,12 +365,12 @@ def main():
         rsum += float(rh.sum())
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
+    stats = reduce_episode_stats({"reward_sum": rsum, "env_steps": n * args.e2e_steps},
+                                 device=dev)  # the optional NCCL stats reduction
     if world > 1:
-        t = torch.tensor([e2e_s, rsum], dtype=torch.float64, device=dev)
-        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
-        stats = torch.tensor([rsum], dtype=torch.float64, device=dev)
-        dist.all_reduce(stats)  # the optional episode-statistics reduction
-        e2e_s, rsum = float(t[0].item()), float(stats.item())
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
     e2e_value = n_total * args.e2e_steps / e2e_s
     eb.check()
 
@@ -385,7 +390,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "env-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform-random policy actions; shipped map"
                     + (" / generated random map" if args.config == "c5" else "") + ")",
             "config": {"workload": CONFIGS[args.config][3], "env": spec.id,
@@ -395,7 +400,8 @@ def main():
                              f"({ring * frame_bytes / 2**20:.0f} MiB > 2x L2)"},
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 9,
-                    "api": "batch_step(host numpy actions, reuse=True) + rewards/dones .cpu()"},
+                    "api": "batch_step(host numpy actions, reuse=True) + rewards/dones .cpu()",
+                    "episode_stats": stats},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "batch_kernel (fused step; avg launch = graph replay / K)",

@@ -23,6 +23,13 @@ PY="${PYTHON:-python3}"
 rm -rf "$OUT.tmp"
 mkdir -p "$OUT.tmp"
 cp -r "$REF" "$OUT.tmp/tilecast"
+# the reference's own test suite, so tests/test_reference_suite.py can run it
+# against the CUDA kernel through the drop-in backend (tests/ref_shim.py)
+if [ -d "$REF/../../tests" ]; then
+  cp -r "$REF/../../tests" "$OUT.tmp/tests"
+  # the tests read maps from <pkg>/src/tilecast/maps
+  mkdir -p "$OUT.tmp/src/tilecast" && cp -r "$REF/maps" "$OUT.tmp/src/tilecast/maps"
+fi
 chmod -R u+w "$OUT.tmp"
 find "$OUT.tmp" -name '__pycache__' -prune -exec rm -rf {} +
 "$PY" -m cython -3 "$OUT.tmp/tilecast/backend/_core.pyx" -o "$OUT.tmp/tilecast/backend/_core.c"

@@ -18,7 +18,11 @@ backend) and records:
 * frames_random.npz  -- render_frame on random maps/poses with doors and
                         entities, plus zbuf;
 * synthetic_maps.npz -- conftest.random_tilemap(random.Random(s)) arrays for
-                        s in 0..19, pinning our synthetic-map generator.
+                        s in 0..19, pinning our synthetic-map generator;
+* tables.npz         -- build_tables output (tables.py:92-184) of every
+                        registered env, pinning our registry + map parser.
+
+``python tests/golden/make_golden.py tables`` regenerates only tables.npz.
 """
 
 from __future__ import annotations
@@ -193,5 +197,22 @@ def _pack_map(t) -> np.ndarray:
     return np.array(out, dtype=np.int64)
 
 
+def export_tables() -> None:
+    from tilecast.suite import make_env, registered_ids
+    out = {}
+    fields = ("kind", "wcol", "didx", "eat", "dcol", "dlock", "ekind", "ecol", "epx", "epy",
+              "spx", "spy", "goal_ent", "dirs", "pal", "door_rgb", "key_rgb", "goal_rgb",
+              "med_box", "med_cross", "ceil_rgb", "floor_rgb", "coef", "fc", "ic", "legal")
+    for env in registered_ids():
+        t = make_env(env).tables
+        for f in fields:
+            out[f"{env}|{f}"] = getattr(t, f)
+    np.savez_compressed(HERE / "tables.npz", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["tables"]:
+        export_tables()
+    else:
+        main()
+        export_tables()
