@@ -132,7 +132,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(cfg, budget_s=10.0):
+def cpu_baseline(cfg, budget_s=12.0):
     """The reference's own CPU kernel (oracle/_ref, Cython+OpenMP) -- or the
     oracle port when _ref is absent -- on this host's cores, over a bounded
     sample of the workload (same spec, same env count, a few steps)."""
@@ -156,7 +156,7 @@ def cpu_baseline(cfg, budget_s=10.0):
         finally:
             if str(ref_dir) in sys.path:
                 sys.path.remove(str(ref_dir))
-    max_steps = 400
+    max_steps = 3000
     acts_all = tc.policy_actions(spec, n, max_steps + 1, 0)
     if kind == "reference":
         rspec = ref.make_env(*([CONFIGS[cfg][0]]), **CONFIGS[cfg][1])
