@@ -106,6 +106,8 @@ struct SpecDev {
   int sealed;        // 1 = map rim is all wall (rays cannot escape)
   int mirror;        // 1 = mirrored-band SWAR compose (even H <= 254, W % 16 == 0)
   int mir_rpi;       // rows per warp pass in the mirror compose (32 / (W/16), >= 1)
+  int direct;        // 1 = mirror compose stores straight to HBM (no TMA staging)
+  int o_t0, o_b0, o_t8, o_wrgb, o_zbuf, o_gdep, o_recs, o_band;  // WarpSmem offsets
   int warp_smem;     // bytes of per-warp shared memory
 };
 
@@ -301,11 +303,11 @@ __device__ __forceinline__ int sprite_mask(int kd, double aa, double ea, double 
 // (:274-304) for each tile. Equivalent to the reference's two passes: a
 // door's open flag only affects its own tile (one door record per door
 // cell), and touch never skips a tile that blocked would test. Returns the
-// door events; `blk` = blocked after the doors were touched.
-__device__ __noinline__ uint32_t scan_tiles(const SpecDev& S, const uint32_t* __restrict__ cell,
-                                            const uint32_t* __restrict__ solid, uint32_t& dmask,
+// door events; result packs (door mask, events, blocked-after-touch).
+__device__ __noinline__ uint64_t scan_tiles(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                            const uint32_t* __restrict__ solid, uint32_t dmask,
                                             double cx, double cy, double radius, uint32_t inv,
-                                            bool touch, bool& blk) {
+                                            bool touch) {
   uint32_t events = 0;
   bool b = false;
   const int tx0 = (int)floor(cx - radius), tx1 = (int)floor(cx + radius);
@@ -337,12 +339,12 @@ __device__ __noinline__ uint32_t scan_tiles(const SpecDev& S, const uint32_t* __
       if ((code & ~dmask) != 0u || code == 0xffffffffu) b = true;
     }
   }
-  blk = b;
-  return events;
+  // packed result: new door mask | events << 32 | blocked << 63
+  return (uint64_t)dmask | ((uint64_t)events << 32) | ((uint64_t)(b ? 1 : 0) << 63);
 }
 
 // _pycore.py:390-414: draws in the contract order spawn, heading, goal
-__device__ __noinline__ void reset_draws(const SpecDev& S, Env& e) {
+__device__ __forceinline__ void reset_draws(const SpecDev& S, Env& e) {
   unsigned long long ctr = e.rctr;
   uint64_t v = draw_below(e.rkey, ctr, (uint64_t)S.n_spawns);
   e.x = S.spx[v];
@@ -404,8 +406,10 @@ __device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_
       if (ax == 2 && !validate) break;
       const double cx = ax == 0 ? x + mvx : x;
       const double cy = ax == 1 ? y + mvy : y;
-      bool blk;
-      o.events |= scan_tiles(S, cell, solid, e.dmask, cx, cy, radius, e.inv, ax < 2, blk);
+      const uint64_t r = scan_tiles(S, cell, solid, e.dmask, cx, cy, radius, e.inv, ax < 2);
+      e.dmask = (uint32_t)r;
+      o.events |= (uint32_t)(r >> 32) & 0x3ffu;
+      const bool blk = (r >> 63) != 0;
       if (ax == 0 && !blk) x = cx;
       if (ax == 1 && !blk) y = cy;
       if (ax == 2 && blk) o.violation = 1;
@@ -491,45 +495,44 @@ __device__ __forceinline__ void bulk_wait_all() {
 //   recs: SpriteRec[E]
 //   band buffers: 2 x band_stride
 struct WarpSmem {
-  uint16_t* t0;
-  uint16_t* b0;
-  uint8_t* t8;  // t0 as bytes (mirror path, obs_h <= 254)
-  uint32_t* wrgb;
-  double* zbuf;
-  double* gdep;
-  double* glat;
-  int* gent;
-  SpriteRec* recs;
-  uint8_t* band[4];
+  // one pointer per warp; the regions sit at host-computed offsets carried
+  // in SpecDev (constant-bank operands), so the compose / ray / sprite code
+  // does not keep a dozen 64-bit pointers live in registers
+  uint8_t* base;
+  __device__ __forceinline__ uint16_t* t0(const SpecDev& S) const { return (uint16_t*)(base + S.o_t0); }
+  __device__ __forceinline__ uint16_t* b0(const SpecDev& S) const { return (uint16_t*)(base + S.o_b0); }
+  __device__ __forceinline__ uint8_t* t8(const SpecDev& S) const { return base + S.o_t8; }
+  __device__ __forceinline__ uint32_t* wrgb(const SpecDev& S) const { return (uint32_t*)(base + S.o_wrgb); }
+  __device__ __forceinline__ double* zbuf(const SpecDev& S) const { return (double*)(base + S.o_zbuf); }
+  __device__ __forceinline__ double* gdep(const SpecDev& S) const { return (double*)(base + S.o_gdep); }
+  __device__ __forceinline__ SpriteRec* recs(const SpecDev& S) const { return (SpriteRec*)(base + S.o_recs); }
+  __device__ __forceinline__ uint8_t* band(const SpecDev& S, int k) const {
+    return base + S.o_band + k * S.band_stride;
+  }
 };
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline int warp_smem_bytes(int obs_w, int n_ent, int band_stride) {
-  const int wp = (obs_w + 3) & ~3;
-  int off = align16(wp * 2) * 2 + align16(wp) + align16(wp * 4) + align16(wp * 8);
-  const int e = n_ent > 0 ? n_ent : 1;
-  off += align16(e * 8) * 2 + align16(e * 4);
-  off += align16(e * (int)sizeof(SpriteRec));
-  off += 4 * band_stride;
-  return off;
+// per-warp shared-memory layout; returns the window size. nbands = staging
+// buffers (0 for the direct-store compose).
+__host__ inline int warp_smem_layout(SpecDev& d, int nbands) {
+  const int wp = (d.obs_w + 15) & ~15;
+  const int e = d.n_ent > 0 ? d.n_ent : 1;
+  int off = 0;
+  d.o_t0 = off; off += align16(wp * 2);
+  d.o_b0 = off; off += align16(wp * 2);
+  d.o_t8 = off; off += align16(wp);
+  d.o_wrgb = off; off += align16(wp * 4);
+  d.o_zbuf = off; off += align16(wp * 8);
+  d.o_gdep = off; off += align16(e * 8);
+  d.o_recs = off; off += align16(e * (int)sizeof(SpriteRec));
+  d.o_band = off; off += nbands * d.band_stride;
+  return align16(off);
 }
 
-__device__ inline WarpSmem carve(uint8_t* base, int obs_w, int n_ent, int band_stride) {
+__device__ inline WarpSmem carve(uint8_t* base) {
   WarpSmem m;
-  const int wp = (obs_w + 3) & ~3;
-  const int e = n_ent > 0 ? n_ent : 1;
-  uint8_t* p = base;
-  m.t0 = (uint16_t*)p; p += align16(wp * 2);
-  m.b0 = (uint16_t*)p; p += align16(wp * 2);
-  m.t8 = p; p += align16(wp);
-  m.wrgb = (uint32_t*)p; p += align16(wp * 4);
-  m.zbuf = (double*)p; p += align16(wp * 8);
-  m.gdep = (double*)p; p += align16(e * 8);
-  m.glat = (double*)p; p += align16(e * 8);
-  m.gent = (int*)p; p += align16(e * 4);
-  m.recs = (SpriteRec*)p; p += align16(e * (int)sizeof(SpriteRec));
-  for (int k = 0; k < 4; k++) { m.band[k] = p; p += band_stride; }
+  m.base = base;
   return m;
 }
 
@@ -651,25 +654,25 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
       continue;
     }
     const double perp = r.xs ? r.sdx - r.ddx : r.sdy - r.ddy;
-    sm.zbuf[c] = perp;
+    sm.zbuf(S)[c] = perp;
     if (zbuf_out) zbuf_out[c] = perp;
     // _pycore.py:162-178
     const double shade = 1.0 / (1.0 + atten * perp);
     const uint32_t cw = cell[r.idx];
     const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
                                                                      : S.pal[cw & 0xffu];
-    sm.wrgb[c] = rgb_scale(base, shade);
+    sm.wrgb(S)[c] = rgb_scale(base, shade);
     double lh_f = (double)H / perp;
     if (lh_f > 1e9) lh_f = 1e9;
     const int half = (int)lh_f / 2;
     const int top = h2 - half, bot = h2 + half;
-    sm.t0[c] = (uint16_t)(top > 0 ? top : 0);
-    sm.t8[c] = (uint8_t)(top > 0 ? top : 0);
-    sm.b0[c] = (uint16_t)(bot < H ? bot : H);
+    sm.t0(S)[c] = (uint16_t)(top > 0 ? top : 0);
+    sm.t8(S)[c] = (uint8_t)(top > 0 ? top : 0);
+    sm.b0(S)[c] = (uint16_t)(bot < H ? bot : H);
   }
   // pad columns so 4-wide loads past W read harmless data
   if (lane < ((W + 3) & ~3) - W) {
-    sm.t0[W + lane] = (uint16_t)h2; sm.b0[W + lane] = (uint16_t)h2; sm.wrgb[W + lane] = 0;
+    sm.t0(S)[W + lane] = (uint16_t)h2; sm.b0(S)[W + lane] = (uint16_t)h2; sm.wrgb(S)[W + lane] = 0;
   }
   if (!CHECKED) return TC_ST_OK;
   const int first_bad = warp_min(bad_col);
@@ -684,7 +687,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
 // here; the survivors keep their relative order, so the stable far->near
 // sort (= the reference's insertion sort, :210-217) of the survivors is the
 // reference's order restricted to sprites that draw. Returns the survivor
-// count m; records land in sm.recs[0..m) in draw order.
+// count m; records land in sm.recs(S)[0..m) in draw order.
 __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm, const Env& e,
                                             double planex, double planey,
                                             unsigned long long* __restrict__ spritevis_out) {
@@ -734,7 +737,7 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         if (vbot - vtop <= 0 || r0 >= r1) continue;
         bool any = false;
         for (int c = lane; c < W; c += 32) {
-          if (!(sm.zbuf[c] <= d)) {
+          if (!(sm.zbuf(S)[c] <= d)) {
             const double a = (S.coef[c] - ks) / halfk;
             any |= !(a <= -1.0 || a >= 1.0);
           }
@@ -756,8 +759,8 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
                               : r.kd == K_GOAL ? S.goal_rgb : S.med_cross;
           r.s1 = rgb_scale(m1, shade);
           r.s2 = rgb_scale(S.med_box, shade);
-          sm.gdep[m] = d;
-          sm.recs[m] = r;  // gathered (entity) order
+          sm.gdep(S)[m] = d;
+          sm.recs(S)[m] = r;  // gathered (entity) order
         }
         vis |= 1ULL << en;
         m++;
@@ -772,24 +775,24 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
     SpriteRec mine;
     int rank = 0;
     if (lane < m) {
-      mine = sm.recs[lane];
-      const double d = sm.gdep[lane];
+      mine = sm.recs(S)[lane];
+      const double d = sm.gdep(S)[lane];
       for (int j = 0; j < m; j++) {
-        const double dj = sm.gdep[j];
+        const double dj = sm.gdep(S)[j];
         rank += (dj > d) || (dj == d && j < lane);
       }
     }
     __syncwarp();
-    if (lane < m) sm.recs[rank] = mine;
+    if (lane < m) sm.recs(S)[rank] = mine;
     // m > 32 survivors: rare (capacity 64); sort the tail serially
     if (m > 32) {
       __syncwarp();
       if (lane == 0) {
         for (int i = 1; i < m; i++) {
-          const SpriteRec it = sm.recs[i];
+          const SpriteRec it = sm.recs(S)[i];
           int j = i;
-          while (j > 0 && sm.recs[j - 1].dep < it.dep) { sm.recs[j] = sm.recs[j - 1]; j--; }
-          sm.recs[j] = it;
+          while (j > 0 && sm.recs(S)[j - 1].dep < it.dep) { sm.recs(S)[j] = sm.recs(S)[j - 1]; j--; }
+          sm.recs(S)[j] = it;
         }
       }
     }
@@ -813,7 +816,7 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
   const int lane = threadIdx.x & 31;
   const int W = S.obs_w, row_bytes = W * 3;
   for (int s = 0; s < m; s++) {
-    const SpriteRec r = sm.recs[s];
+    const SpriteRec r = sm.recs(S)[s];
     const double denom = (double)r.denom;
     const bool key = r.kd == K_KEY;
     for (int half = 0; half < 2; half++) {
@@ -831,7 +834,7 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
         vis[j] = false;
         aa[j] = 0.0;
         ea[j] = 0.0;
-        if (c < W && !(sm.zbuf[c] <= r.dep)) {
+        if (c < W && !(sm.zbuf(S)[c] <= r.dep)) {
           const double a = (S.coef[c] - r.ks) / r.halfk;
           if (!(a <= -1.0 || a >= 1.0)) {
             vis[j] = true;
@@ -952,15 +955,15 @@ __device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& s
                    fw2 = __byte_perm(F, F, 0x6542);
     for (int r_lo = 0; r_lo < h2; r_lo += B, buf ^= 1) {
       const int rows = min(B, h2 - r_lo);
-      uint8_t* top = sm.band[2 * buf];
-      uint8_t* bot = sm.band[2 * buf + 1];
+      uint8_t* top = sm.band(S, 2 * buf);
+      uint8_t* bot = sm.band(S, 2 * buf + 1);
       const int r_bot = H - r_lo - rows;  // first frame row of the bottom band
       if (lane == 0 && bulk_pending > 1) bulk_wait_read_le1();
       __syncwarp();
       if (rowoff < RPI) {
         for (int cg = cg0; cg < CG; cg += 32) {
-          const uint4 T = *reinterpret_cast<const uint4*>(sm.t8 + 16 * cg);
-          const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb + 16 * cg);
+          const uint4 T = *reinterpret_cast<const uint4*>(sm.t8(S) + 16 * cg);
+          const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 16 * cg);
           uint32_t Wd[12];
 #pragma unroll
           for (int j = 0; j < 4; j++) {
@@ -1012,6 +1015,72 @@ __device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& s
   __syncwarp();
 }
 
+// Mirrored compose written straight to HBM from registers (no staging):
+// each lane stores its 48 bytes per row as 3 streaming 16-byte stores; the
+// sprite pass then overwrites its pixels with byte stores after a __syncwarp
+// (which orders the warp's memory operations).
+template <int NC>
+__device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& sm, int m,
+                                              uint8_t* __restrict__ frame, const LaneGeo& lg) {
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
+  const int row_bytes = W * 3;
+  const int CG = W >> 4;
+  const int RPI = S.mir_rpi;
+  const int rowoff = lg.rowoff;
+  const uint32_t C = S.ceil_rgb, F = S.floor_rgb;
+  const uint32_t cw0 = __byte_perm(C, C, 0x4210), cw1 = __byte_perm(C, C, 0x5421),
+                 cw2 = __byte_perm(C, C, 0x6542);
+  const uint32_t fw0 = __byte_perm(F, F, 0x4210), fw1 = __byte_perm(F, F, 0x5421),
+                 fw2 = __byte_perm(F, F, 0x6542);
+  if (rowoff < RPI) {
+    for (int cg = lg.cg0; cg < CG; cg += 32) {
+      const uint4 T = *reinterpret_cast<const uint4*>(sm.t8(S) + 16 * cg);
+      const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 16 * cg);
+      uint32_t Wd[12];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const uint4 w = wp[j];
+        Wd[3 * j + 0] = __byte_perm(w.x, w.y, 0x4210);
+        Wd[3 * j + 1] = __byte_perm(w.y, w.z, 0x5421);
+        Wd[3 * j + 2] = __byte_perm(w.z, w.w, 0x6542);
+      }
+      const uint32_t Tj[4] = {T.x, T.y, T.z, T.w};
+      uint8_t* top = frame + (size_t)rowoff * row_bytes + cg * 48;
+      uint8_t* bot = frame + (size_t)(H - 1 - rowoff) * row_bytes + cg * 48;
+      const size_t step = (size_t)RPI * row_bytes;
+      for (int r = rowoff; r < h2; r += RPI, top += step, bot -= step) {
+        const uint32_t R = 0x80808080u + (uint32_t)r * 0x01010101u;
+        uint32_t tw[12], bw[12];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const uint32_t D = R - Tj[j];
+          const uint32_t m0 = prmt_sx(D, 0x9888), m1 = prmt_sx(D, 0xAA99),
+                         m2 = prmt_sx(D, 0xBBBA);
+          tw[3 * j + 0] = (m0 & Wd[3 * j + 0]) | (~m0 & cw0);
+          tw[3 * j + 1] = (m1 & Wd[3 * j + 1]) | (~m1 & cw1);
+          tw[3 * j + 2] = (m2 & Wd[3 * j + 2]) | (~m2 & cw2);
+          bw[3 * j + 0] = (m0 & Wd[3 * j + 0]) | (~m0 & fw0);
+          bw[3 * j + 1] = (m1 & Wd[3 * j + 1]) | (~m1 & fw1);
+          bw[3 * j + 2] = (m2 & Wd[3 * j + 2]) | (~m2 & fw2);
+        }
+        uint4* dt = reinterpret_cast<uint4*>(top);
+        uint4* db = reinterpret_cast<uint4*>(bot);
+        __stcs(dt + 0, make_uint4(tw[0], tw[1], tw[2], tw[3]));
+        __stcs(dt + 1, make_uint4(tw[4], tw[5], tw[6], tw[7]));
+        __stcs(dt + 2, make_uint4(tw[8], tw[9], tw[10], tw[11]));
+        __stcs(db + 0, make_uint4(bw[0], bw[1], bw[2], bw[3]));
+        __stcs(db + 1, make_uint4(bw[4], bw[5], bw[6], bw[7]));
+        __stcs(db + 2, make_uint4(bw[8], bw[9], bw[10], bw[11]));
+      }
+    }
+  }
+  if (m > 0) {
+    __syncwarp();
+    draw_sprites<NC>(S, sm, m, frame, 0, nullptr, 0, H);
+  }
+  __syncwarp();
+}
+
 // Phase 3: compose the frame in staged bands, draw sprites, ship with TMA.
 template <int NC>
 __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSmem& sm, int m,
@@ -1020,7 +1089,8 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
   const int lane = threadIdx.x & 31;
   const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
   if (S.mirror) {
-    mirror_bands<NC, true>(S, sm, m, frame, bulk_pending, buf, lg);
+    if (S.direct) mirror_direct<NC>(S, sm, m, frame, lg);
+    else mirror_bands<NC, true>(S, sm, m, frame, bulk_pending, buf, lg);
     return;
   }
 
@@ -1029,7 +1099,7 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
   // wall/floor, [bmax,H) floor everywhere (t0 <= h2 <= b0 per column).
   int tlo = 0x7fffffff, thi = 0, blo = 0x7fffffff, bhi = 0;
   for (int c = lane; c < W; c += 32) {
-    const int t = sm.t0[c], b = sm.b0[c];
+    const int t = sm.t0(S)[c], b = sm.b0(S)[c];
     tlo = min(tlo, t); thi = max(thi, t); blo = min(blo, b); bhi = max(bhi, b);
   }
   const int tmin = warp_min(tlo), tmax = warp_max(thi);
@@ -1050,16 +1120,16 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
   for (int r_lo = 0; r_lo < H; r_lo += B, buf ^= 1) {
     const int rows = min(B, H - r_lo);
     const int r_end = r_lo + rows;
-    uint8_t* band = sm.band[buf];
+    uint8_t* band = sm.band(S, buf);
     // the buffer we are about to overwrite was shipped two bands ago
     if (S.bulk && lane == 0 && bulk_pending > 1) bulk_wait_read_le1();
     __syncwarp();
     if (S.quads) {
       if (rsub < G) {
         for (int q = q_first; q < Q; q += 32) {
-          const uint2 t4 = *reinterpret_cast<const uint2*>(sm.t0 + 4 * q);
-          const uint2 b4 = *reinterpret_cast<const uint2*>(sm.b0 + 4 * q);
-          const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb + 4 * q);
+          const uint2 t4 = *reinterpret_cast<const uint2*>(sm.t0(S) + 4 * q);
+          const uint2 b4 = *reinterpret_cast<const uint2*>(sm.b0(S) + 4 * q);
+          const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb(S) + 4 * q);
           const int t0 = t4.x & 0xffff, t1 = t4.x >> 16, t2 = t4.y & 0xffff, t3 = t4.y >> 16;
           const int b0 = b4.x & 0xffff, b1 = b4.x >> 16, b2 = b4.y & 0xffff, b3 = b4.y >> 16;
           const uint32_t w0w = __byte_perm(w4.x, w4.y, 0x4210),
@@ -1090,7 +1160,7 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
       for (int p = lane; p < items; p += 32) {
         const int rr = p / W, c = p - rr * W;
         const uint32_t row = (uint32_t)(r_lo + rr);
-        const uint32_t col = row < sm.t0[c] ? C : (row < sm.b0[c] ? sm.wrgb[c] : F);
+        const uint32_t col = row < sm.t0(S)[c] ? C : (row < sm.b0(S)[c] ? sm.wrgb(S)[c] : F);
         uint8_t* d = band + rr * row_bytes + c * 3;
         d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
       }
@@ -1199,7 +1269,8 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
 // MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387
 template <int NC>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
-batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutDev out,
+batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
+             const long long* __restrict__ actions, const __grid_constant__ OutDev out,
              long long n, int mode, int auto_reset, int validate,
              tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1208,8 +1279,7 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
   const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
   const uint32_t *cell, *solid;
   stage_map(S, smap, cell, solid);
-  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
-                            S.band_stride);
+  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
   const LaneGeo lg = lane_geo(S);
   int bulk_pending = 0, buf = 0;
@@ -1297,7 +1367,8 @@ batch_kernel(SpecDev S, StateDev st, const long long* __restrict__ actions, OutD
 // auto-reset; the env's state stays in registers across steps.
 template <int NC>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
-rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
+rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
+               const __grid_constant__ OutDev out, long long n, const __grid_constant__ RolloutArgs ra,
                tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1305,8 +1376,7 @@ rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
   const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
   const uint32_t *cell, *solid;
   stage_map(S, smap, cell, solid);
-  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
-                            S.band_stride);
+  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
   const LaneGeo lg = lane_geo(S);
   int bulk_pending = 0, buf = 0;
@@ -1355,7 +1425,8 @@ rollout_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
 // footprint exceeds the instruction cache; one phase's does not).
 template <int NC, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 3 : 1))
-rollout_phased_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutArgs ra,
+rollout_phased_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
+                      const __grid_constant__ OutDev out, long long n, const __grid_constant__ RolloutArgs ra,
                       tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1363,8 +1434,7 @@ rollout_phased_kernel(SpecDev S, StateDev st, OutDev out, long long n, RolloutAr
   const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
   const uint32_t *cell, *solid;
   stage_map(S, smap, cell, solid);
-  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem, S.obs_w, S.n_ent,
-                            S.band_stride);
+  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
   const LaneGeo lg = lane_geo(S);
   int bulk_pending = 0, buf = 0;
@@ -1626,7 +1696,9 @@ int launch_geometry(tc_spec* s) {
   if (rows > d.obs_h) rows = d.obs_h;
   d.band_rows = rows;
   d.band_stride = align16(rows * row_bytes);
-  d.warp_smem = align16(warp_smem_bytes(d.obs_w, d.n_ent, d.band_stride));
+  const char* dr = getenv("TILECAST_DIRECT");
+  d.direct = (dr && atoi(dr) && d.mirror) ? 1 : 0;
+  d.warp_smem = warp_smem_layout(d, d.direct ? 0 : (d.mirror ? 4 : 2));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
   const size_t map_bytes = d.smem_map ? (size_t)align16(d.h * d.w * 8) : 0;
   s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * d.warp_smem;
