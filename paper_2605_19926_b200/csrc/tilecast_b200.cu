@@ -57,9 +57,6 @@ constexpr uint64_t MIX2 = 0x94D049BB133111EBULL;
 constexpr uint64_t SPLIT_SALT = 0x3C6EF372FE94F82AULL;
 
 constexpr int WARPS_PER_CTA = 4;
-#ifndef TC_EXPERIMENT
-#define TC_EXPERIMENT 0  // perf experiments only: 1 = skip sprites, 2 = skip sprite draw
-#endif
 #ifndef TC_TRACE
 #define TC_TRACE 0  // perf experiments only: per-env phase timestamps
 #endif
@@ -105,8 +102,11 @@ struct SpecDev {
   int bulk;          // 1 = frame rows are 16-byte multiples (TMA bulk store)
   int sealed;        // 1 = map rim is all wall (rays cannot escape)
   int mirror;        // 1 = mirrored-band SWAR compose (even H <= 254, W % 16 == 0)
-  int mir_rpi;       // rows per warp pass in the mirror compose (32 / (W/16), >= 1)
+  int mir_rpi;       // rows per 32-lane pass in the mirror compose (32 / (W/16), >= 1)
+  int mir_rpi16;     // same for 16-lane groups
+  int group;         // lanes per env: 32 (one env per warp) or 16 (two per warp)
   int direct;        // 1 = mirror compose stores straight to HBM (no TMA staging)
+  int npairs;        // mirror path: staged band pairs in flight (2..4)
   int o_t0, o_b0, o_t8, o_wrgb, o_zbuf, o_gdep, o_recs, o_band;  // WarpSmem offsets
   int warp_smem;     // bytes of per-warp shared memory
 };
@@ -171,7 +171,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #define TRACE(i, slot)                                                   \
   do {                                                                   \
-    if (g_trace && (threadIdx.x & 31) == 0) g_trace[(i) * 8 + (slot)] = gtime(); \
+    if (g_trace && (threadIdx.x & (G - 1)) == 0) g_trace[(i) * 8 + (slot)] = gtime(); \
   } while (0)
 #else
 #define TRACE(i, slot) do { } while (0)
@@ -481,6 +481,12 @@ __device__ __forceinline__ uint32_t prmt_sx(uint32_t a, uint32_t sel) {
   asm("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(a), "r"(sel));
   return d;
 }
+// wait until at most n bulk groups still read shared memory (n = 1..3)
+__device__ __forceinline__ void bulk_wait_read_le(int n) {
+  if (n <= 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  else if (n == 2) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+  else asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_read_le1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
@@ -536,16 +542,38 @@ __device__ inline WarpSmem carve(uint8_t* base) {
   return m;
 }
 
-__device__ __forceinline__ int warp_min(int v) {
+// A group of G lanes (G = 32: one env per warp; G = 16: two envs per warp,
+// one per half) and its collectives. Masks are the group's own, so the two
+// halves of a warp may diverge freely.
+template <int G>
+struct Grp {
+  int lane;        // lane within the group
+  int shift;       // bit offset of the group inside the warp
+  unsigned mask;   // member mask
+  __device__ __forceinline__ Grp() {
+    const int l = threadIdx.x & 31;
+    lane = l & (G - 1);
+    shift = l & ~(G - 1) & 31;
+    mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << shift);
+  }
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    return (__ballot_sync(mask, p) & mask) >> shift;
+  }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  template <class T>
+  __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src, G); }
+  __device__ __forceinline__ int min(int v) const {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ int warp_max(int v) {
+    for (int o = G / 2; o > 0; o >>= 1) v = ::min(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+  }
+  __device__ __forceinline__ int max(int v) const {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
+    for (int o = G / 2; o > 0; o >>= 1) v = ::max(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+  }
+};
 
 // One DDA march, _pycore.py:38-96. `solid` holds per-cell stop codes
 // (wall = ~0u, door d = 1u << d, floor = 0): a ray stops in a cell iff
@@ -625,19 +653,20 @@ __device__ __forceinline__ March march(const uint32_t* __restrict__ solid, int m
 // Wall pass: lane L casts the rays of columns L + 32j; per-column spans,
 // colours and zbuf go to shared memory (_pycore.py:153-190). Returns the
 // status of the first failing column (warp-uniform).
-template <int NC, bool CHECKED>
+template <int NC, bool CHECKED, int G>
 __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __restrict__ cell,
                                          const uint32_t* __restrict__ solid,
                                          const WarpSmem& sm, const Env& e, double planex,
                                          double planey, double* __restrict__ zbuf_out,
                                          int32_t* __restrict__ rayinfo) {
-  const int lane = threadIdx.x & 31;
+  const Grp<G> g;
+  const int lane = g.lane;
   const int W = S.obs_w, H = S.obs_h, h2 = H / 2, mw = S.w;
   const int ox = (int)floor(e.x), oy = (int)floor(e.y);
   const double atten = S.fc[FC_ATTEN];
   int bad_col = 0x7fffffff, bad_status = TC_ST_OK;
 #pragma unroll 1
-  for (int c = lane; c < W; c += 32) {
+  for (int c = lane; c < W; c += G) {
     const double k = S.coef[c];
     const double rx = e.dx + planex * k;
     const double ry = e.dy + planey * k;
@@ -675,9 +704,9 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     sm.t0(S)[W + lane] = (uint16_t)h2; sm.b0(S)[W + lane] = (uint16_t)h2; sm.wrgb(S)[W + lane] = 0;
   }
   if (!CHECKED) return TC_ST_OK;
-  const int first_bad = warp_min(bad_col);
+  const int first_bad = g.min(bad_col);
   if (first_bad == 0x7fffffff) return TC_ST_OK;
-  return __shfl_sync(0xffffffffu, bad_status, first_bad & 31);
+  return g.shfl(bad_status, first_bad % G);
 }
 
 // Sprite gather (entity order, _pycore.py:192-209) and per-sprite
@@ -688,10 +717,12 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
 // sort (= the reference's insertion sort, :210-217) of the survivors is the
 // reference's order restricted to sprites that draw. Returns the survivor
 // count m; records land in sm.recs(S)[0..m) in draw order.
+template <int G>
 __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm, const Env& e,
                                             double planex, double planey,
                                             unsigned long long* __restrict__ spritevis_out) {
-  const int lane = threadIdx.x & 31;
+  const Grp<G> g;
+  const int lane = g.lane;
   const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
   int m = 0;
   unsigned long long vis = 0;
@@ -699,7 +730,7 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
   if (det != 0.0) {
     const double invdet = 1.0 / det;
     const double atten = S.fc[FC_ATTEN], spk = S.fc[FC_SPRITE_K];
-    for (int base = 0; base < S.n_ent; base += 32) {
+    for (int base = 0; base < S.n_ent; base += G) {
       const int ent = base + lane;
       bool keep = false;
       double lat = 0.0, dep = 0.0;
@@ -715,34 +746,34 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         // rounding, so every column's |a| >= 1 and the sprite draws nothing
         if (keep && fabs(lat) > (dep + S.fc[FC_SPRITE_K]) * (1.0 + 1e-6)) keep = false;
       }
-      uint32_t bal = __ballot_sync(0xffffffffu, keep);
+      uint32_t bal = g.ballot(keep);
       while (bal) {  // warp-uniform walk over the gathered sprites
         const int src = __ffs(bal) - 1;
         bal &= bal - 1u;
-        const double d = __shfl_sync(0xffffffffu, dep, src);
-        const double l = __shfl_sync(0xffffffffu, lat, src);
+        const double d = g.shfl(dep, src);
+        const double l = g.shfl(lat, src);
         // the four per-sprite quotients, one per lane (same operands and
         // order as _pycore.py:220-223), then broadcast
         const double qn = lane == 0 ? (double)H : lane == 1 ? l : lane == 2 ? spk : 1.0;
         const double qd = lane == 3 ? 1.0 + atten * d : d;
         const double q = qn / qd;
-        double sh_f = __shfl_sync(0xffffffffu, q, 0);
-        const double ks = __shfl_sync(0xffffffffu, q, 1);
-        const double halfk = __shfl_sync(0xffffffffu, q, 2);
-        const double shade = __shfl_sync(0xffffffffu, q, 3);
+        double sh_f = g.shfl(q, 0);
+        const double ks = g.shfl(q, 1);
+        const double halfk = g.shfl(q, 2);
+        const double shade = g.shfl(q, 3);
         if (sh_f > 1e9) sh_f = 1e9;
         const int vhalf = (int)sh_f / 2;
         const int vtop = h2 - vhalf, vbot = h2 + vhalf;
         const int r0 = vtop > 0 ? vtop : 0, r1 = vbot < H ? vbot : H;
         if (vbot - vtop <= 0 || r0 >= r1) continue;
         bool any = false;
-        for (int c = lane; c < W; c += 32) {
+        for (int c = lane; c < W; c += G) {
           if (!(sm.zbuf(S)[c] <= d)) {
             const double a = (S.coef[c] - ks) / halfk;
             any |= !(a <= -1.0 || a >= 1.0);
           }
         }
-        if (!__any_sync(0xffffffffu, any)) continue;
+        if (!g.any(any)) continue;
         const int en = base + src;
         if (lane == 0) {
           SpriteRec r;
@@ -771,7 +802,7 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
   if (m > 1) {
     // stable far -> near: rank = #deeper + #equal-and-earlier; permute via
     // registers (all lanes read before any lane writes)
-    __syncwarp();
+    g.sync();
     SpriteRec mine;
     int rank = 0;
     if (lane < m) {
@@ -782,11 +813,11 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         rank += (dj > d) || (dj == d && j < lane);
       }
     }
-    __syncwarp();
+    g.sync();
     if (lane < m) sm.recs(S)[rank] = mine;
-    // m > 32 survivors: rare (capacity 64); sort the tail serially
-    if (m > 32) {
-      __syncwarp();
+    // m > G survivors: rare (capacity 64); sort the tail serially
+    if (m > G) {
+      g.sync();
       if (lane == 0) {
         for (int i = 1; i < m; i++) {
           const SpriteRec it = sm.recs(S)[i];
@@ -797,7 +828,7 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
       }
     }
   }
-  __syncwarp();
+  g.sync();
   return m;
 }
 
@@ -809,11 +840,12 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
 // (v - 0.30) / 0.18) is computed lane-parallel -- lane k divides for row
 // ra + k -- and broadcast with shuffles. Same doubles, same comparisons as
 // the reference, ~1 division per 32 rows instead of 1 per row.
-template <int NC>
+template <int NC, int G>
 __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& sm, int m,
                                              uint8_t* bandA, int rA, uint8_t* bandB, int rB,
                                              int rows) {
-  const int lane = threadIdx.x & 31;
+  const Grp<G> g;
+  const int lane = g.lane;
   const int W = S.obs_w, row_bytes = W * 3;
   for (int s = 0; s < m; s++) {
     const SpriteRec r = sm.recs(S)[s];
@@ -830,7 +862,7 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
       bool anyv = false;
 #pragma unroll
       for (int j = 0; j < NC; j++) {
-        const int c = lane + 32 * j;
+        const int c = lane + G * j;
         vis[j] = false;
         aa[j] = 0.0;
         ea[j] = 0.0;
@@ -844,18 +876,18 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
         }
         anyv |= vis[j];
       }
-      if (!__any_sync(0xffffffffu, anyv)) continue;
-      for (int r32 = ra; r32 < rb; r32 += 32) {
-        // lane-parallel row terms for rows r32 .. r32+31
+      if (!g.any(anyv)) continue;
+      for (int r32 = ra; r32 < rb; r32 += G) {
+        // lane-parallel row terms for rows r32 .. r32+G-1
         double v_l = 0.0, ev_l = 0.0;
         if (r32 + lane < rb) {
           v_l = ((double)(r32 + lane - r.vtop) + 0.5) / denom;
           if (key) ev_l = (v_l - 0.30) / 0.18;
         }
-        const int nr = min(32, rb - r32);
+        const int nr = min(G, rb - r32);
         for (int k = 0; k < nr; k++) {
-          const double v = __shfl_sync(0xffffffffu, v_l, k);
-          const double ev = __shfl_sync(0xffffffffu, ev_l, k);
+          const double v = g.shfl(v_l, k);
+          const double ev = g.shfl(ev_l, k);
           uint8_t* drow = band + (r32 + k - r_lo) * row_bytes;
 #pragma unroll
           for (int j = 0; j < NC; j++) {
@@ -863,7 +895,7 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
             const int mk = sprite_mask(r.kd, aa[j], ea[j], v, ev);
             if (mk) {
               const uint32_t col = mk == 1 ? r.s1 : r.s2;
-              uint8_t* d = drow + (lane + 32 * j) * 3;
+              uint8_t* d = drow + (lane + G * j) * 3;
               d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
             }
           }
@@ -877,13 +909,14 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
 struct LaneGeo {
   int rowoff, cg0;
 };
+template <int G>
 __device__ __forceinline__ LaneGeo lane_geo(const SpecDev& S) {
-  const int lane = threadIdx.x & 31;
+  const int lane = Grp<G>().lane;
   const int CG = S.obs_w >> 4;
-  LaneGeo g;
-  g.rowoff = (S.mirror && CG < 32) ? lane / CG : 0;
-  g.cg0 = (S.mirror && CG < 32) ? lane - g.rowoff * CG : lane;
-  return g;
+  LaneGeo lg;
+  lg.rowoff = (S.mirror && CG < G) ? lane / CG : 0;
+  lg.cg0 = (S.mirror && CG < G) ? lane - lg.rowoff * CG : lane;
+  return lg;
 }
 
 // 4-pixel group (12 bytes) from 4 packed rgb words
@@ -898,7 +931,7 @@ __device__ __forceinline__ void put_quad(uint32_t* dst, uint32_t p0, uint32_t p1
 // Returns the status of the first failing column (or OK), warp-uniform.
 // _pycore.py:132-271.
 // Phase 1 of rendering: wall pass (spans / zbuf into shared memory).
-template <int NC>
+template <int NC, int G>
 __device__ __forceinline__ int render_walls(const SpecDev& S, const uint32_t* __restrict__ cell,
                                             const uint32_t* __restrict__ solid,
                                             const WarpSmem& sm, const Env& e,
@@ -909,31 +942,32 @@ __device__ __forceinline__ int render_walls(const SpecDev& S, const uint32_t* __
   // fast march when the rim is sealed and the origin is on the grid
   const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h;
   const int st = (S.sealed && inside)
-      ? wall_pass<NC, false>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
-      : wall_pass<NC, true>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo);
-  __syncwarp();
+      ? wall_pass<NC, false, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
+      : wall_pass<NC, true, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo);
+  Grp<G>().sync();
   return st;
 }
 
 // Phase 2: sprite setup; returns the number of sprites that draw.
+template <int G>
 __device__ __forceinline__ int render_sprites(const SpecDev& S, const WarpSmem& sm, const Env& e,
                                               unsigned long long* __restrict__ spritevis_out) {
-  if (S.n_ent == 0 || TC_EXPERIMENT == 1) {
+  if (S.n_ent == 0) {
     if (spritevis_out && (threadIdx.x & 31) == 0) *spritevis_out = 0;
     return 0;
   }
   const double planex = -e.dy * PLANE_HALF_WIDTH;
   const double planey = e.dx * PLANE_HALF_WIDTH;
-  const int m = sprite_setup(S, sm, e, planex, planey, spritevis_out);
-  return TC_EXPERIMENT == 2 ? 0 : m;
+  return sprite_setup<G>(S, sm, e, planex, planey, spritevis_out);
 }
 
 // Mirrored-band compose + sprites + TMA store (see render_frame_out).
-template <int NC, bool SPR>
+template <int NC, bool SPR, int G>
 __device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& sm, int m,
                                              uint8_t* __restrict__ frame, int& bulk_pending,
                                              int& buf, const LaneGeo& lg) {
-  const int lane = threadIdx.x & 31;
+  const Grp<G> g;
+  const int lane = g.lane;
   const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
     // Mirrored bands (even H <= 254, W % 16 == 0). Row r and row H-1-r have
     // the same wall / non-wall pattern (t0 = h2-half, b0 = h2+half), so one
@@ -945,7 +979,7 @@ __device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& s
     const int row_bytes = W * 3;
     const int B = S.band_rows;
     const int CG = W >> 4;
-    const int RPI = S.mir_rpi;
+    const int RPI = G == 32 ? S.mir_rpi : S.mir_rpi16;
     const int rowoff = lg.rowoff;
     const int cg0 = lg.cg0;
     const uint32_t C = S.ceil_rgb, F = S.floor_rgb;
@@ -953,15 +987,17 @@ __device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& s
                    cw2 = __byte_perm(C, C, 0x6542);
     const uint32_t fw0 = __byte_perm(F, F, 0x4210), fw1 = __byte_perm(F, F, 0x5421),
                    fw2 = __byte_perm(F, F, 0x6542);
-    for (int r_lo = 0; r_lo < h2; r_lo += B, buf ^= 1) {
+    const int NP = S.npairs;  // band-pair buffers in flight
+    for (int r_lo = 0; r_lo < h2; r_lo += B, buf = (buf + 1 == NP ? 0 : buf + 1)) {
       const int rows = min(B, h2 - r_lo);
       uint8_t* top = sm.band(S, 2 * buf);
       uint8_t* bot = sm.band(S, 2 * buf + 1);
       const int r_bot = H - r_lo - rows;  // first frame row of the bottom band
-      if (lane == 0 && bulk_pending > 1) bulk_wait_read_le1();
-      __syncwarp();
+      // the pair we overwrite was shipped NP pairs ago
+      if (lane == 0 && bulk_pending >= NP) bulk_wait_read_le(NP - 1);
+      g.sync();
       if (rowoff < RPI) {
-        for (int cg = cg0; cg < CG; cg += 32) {
+        for (int cg = cg0; cg < CG; cg += G) {
           const uint4 T = *reinterpret_cast<const uint4*>(sm.t8(S) + 16 * cg);
           const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 16 * cg);
           uint32_t Wd[12];
@@ -1000,32 +1036,50 @@ __device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& s
         }
       }
       if (SPR && m > 0) {
-        __syncwarp();
-        draw_sprites<NC>(S, sm, m, top, r_lo, bot, r_bot, rows);
+        g.sync();
+        draw_sprites<NC, G>(S, sm, m, top, r_lo, bot, r_bot, rows);
       }
-      bulk_fence();
-      __syncwarp();
-      if (lane == 0) {
-        bulk_copy(frame + (size_t)r_lo * row_bytes, top, (uint32_t)(rows * row_bytes));
-        bulk_copy(frame + (size_t)r_bot * row_bytes, bot, (uint32_t)(rows * row_bytes));
-        bulk_commit();
-        bulk_pending++;
+      if (S.direct == 2) {
+        // coalesced copy-out by the warp: each 16-byte store instruction
+        // covers 512 contiguous bytes (full sectors), generic proxy only
+        g.sync();
+        const int nchunk = rows * row_bytes / 16;
+        const uint4* st4 = reinterpret_cast<const uint4*>(top);
+        const uint4* sb4 = reinterpret_cast<const uint4*>(bot);
+        uint4* gt = reinterpret_cast<uint4*>(frame + (size_t)r_lo * row_bytes);
+        uint4* gb = reinterpret_cast<uint4*>(frame + (size_t)r_bot * row_bytes);
+        for (int k = lane; k < nchunk; k += G) {
+          const uint4 a = st4[k], b = sb4[k];
+          __stcs(gt + k, a);
+          __stcs(gb + k, b);
+        }
+        g.sync();
+      } else {
+        bulk_fence();
+        g.sync();
+        if (lane == 0) {
+          bulk_copy(frame + (size_t)r_lo * row_bytes, top, (uint32_t)(rows * row_bytes));
+          bulk_copy(frame + (size_t)r_bot * row_bytes, bot, (uint32_t)(rows * row_bytes));
+          bulk_commit();
+          bulk_pending++;
+        }
       }
     }
-  __syncwarp();
+  g.sync();
 }
 
 // Mirrored compose written straight to HBM from registers (no staging):
 // each lane stores its 48 bytes per row as 3 streaming 16-byte stores; the
 // sprite pass then overwrites its pixels with byte stores after a __syncwarp
 // (which orders the warp's memory operations).
-template <int NC>
+template <int NC, int G>
 __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& sm, int m,
                                               uint8_t* __restrict__ frame, const LaneGeo& lg) {
+  const Grp<G> g;
   const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
   const int row_bytes = W * 3;
   const int CG = W >> 4;
-  const int RPI = S.mir_rpi;
+  const int RPI = G == 32 ? S.mir_rpi : S.mir_rpi16;
   const int rowoff = lg.rowoff;
   const uint32_t C = S.ceil_rgb, F = S.floor_rgb;
   const uint32_t cw0 = __byte_perm(C, C, 0x4210), cw1 = __byte_perm(C, C, 0x5421),
@@ -1033,7 +1087,7 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
   const uint32_t fw0 = __byte_perm(F, F, 0x4210), fw1 = __byte_perm(F, F, 0x5421),
                  fw2 = __byte_perm(F, F, 0x6542);
   if (rowoff < RPI) {
-    for (int cg = lg.cg0; cg < CG; cg += 32) {
+    for (int cg = lg.cg0; cg < CG; cg += G) {
       const uint4 T = *reinterpret_cast<const uint4*>(sm.t8(S) + 16 * cg);
       const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 16 * cg);
       uint32_t Wd[12];
@@ -1075,22 +1129,23 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
     }
   }
   if (m > 0) {
-    __syncwarp();
-    draw_sprites<NC>(S, sm, m, frame, 0, nullptr, 0, H);
+    g.sync();
+    draw_sprites<NC, G>(S, sm, m, frame, 0, nullptr, 0, H);
   }
-  __syncwarp();
+  g.sync();
 }
 
 // Phase 3: compose the frame in staged bands, draw sprites, ship with TMA.
-template <int NC>
+template <int NC, int G>
 __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSmem& sm, int m,
                                                  uint8_t* __restrict__ frame, int& bulk_pending,
                                                  int& buf, const LaneGeo& lg) {
-  const int lane = threadIdx.x & 31;
+  const Grp<G> g;
+  const int lane = g.lane;
   const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
   if (S.mirror) {
-    if (S.direct) mirror_direct<NC>(S, sm, m, frame, lg);
-    else mirror_bands<NC, true>(S, sm, m, frame, bulk_pending, buf, lg);
+    if (S.direct == 1) mirror_direct<NC, G>(S, sm, m, frame, lg);
+    else mirror_bands<NC, true, G>(S, sm, m, frame, bulk_pending, buf, lg);
     return;
   }
 
@@ -1098,12 +1153,12 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
   // mixed ceiling/wall, [tmax,bmin) wall everywhere, [bmin,bmax) mixed
   // wall/floor, [bmax,H) floor everywhere (t0 <= h2 <= b0 per column).
   int tlo = 0x7fffffff, thi = 0, blo = 0x7fffffff, bhi = 0;
-  for (int c = lane; c < W; c += 32) {
+  for (int c = lane; c < W; c += G) {
     const int t = sm.t0(S)[c], b = sm.b0(S)[c];
     tlo = min(tlo, t); thi = max(thi, t); blo = min(blo, b); bhi = max(bhi, b);
   }
-  const int tmin = warp_min(tlo), tmax = warp_max(thi);
-  const int bmin = warp_min(blo), bmax = warp_max(bhi);
+  const int tmin = g.min(tlo), tmax = g.max(thi);
+  const int bmin = g.min(blo), bmax = g.max(bhi);
 
   const int row_bytes = W * 3;
   const int B = S.band_rows;
@@ -1113,9 +1168,9 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
   const uint32_t f0w = __byte_perm(F, F, 0x4210), f1w = __byte_perm(F, F, 0x5421),
                  f2w = __byte_perm(F, F, 0x6542);
   const int Q = W >> 2;
-  const int G = Q >= 32 ? 1 : 32 / Q;  // row groups per warp
-  const int rsub = Q >= 32 ? 0 : lane / Q;
-  const int q_first = Q >= 32 ? lane : lane - rsub * Q;
+  const int RG = Q >= G ? 1 : G / Q;  // row groups per lane group
+  const int rsub = Q >= G ? 0 : lane / Q;
+  const int q_first = Q >= G ? lane : lane - rsub * Q;
 
   for (int r_lo = 0; r_lo < H; r_lo += B, buf ^= 1) {
     const int rows = min(B, H - r_lo);
@@ -1123,10 +1178,10 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
     uint8_t* band = sm.band(S, buf);
     // the buffer we are about to overwrite was shipped two bands ago
     if (S.bulk && lane == 0 && bulk_pending > 1) bulk_wait_read_le1();
-    __syncwarp();
+    g.sync();
     if (S.quads) {
-      if (rsub < G) {
-        for (int q = q_first; q < Q; q += 32) {
+      if (rsub < RG) {
+        for (int q = q_first; q < Q; q += G) {
           const uint2 t4 = *reinterpret_cast<const uint2*>(sm.t0(S) + 4 * q);
           const uint2 b4 = *reinterpret_cast<const uint2*>(sm.b0(S) + 4 * q);
           const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb(S) + 4 * q);
@@ -1136,28 +1191,28 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
                          w1w = __byte_perm(w4.y, w4.z, 0x5421),
                          w2w = __byte_perm(w4.z, w4.w, 0x6542);
           uint32_t* dst = reinterpret_cast<uint32_t*>(band + rsub * row_bytes + q * 12);
-          const int dstep = G * row_bytes / 4;
+          const int dstep = RG * row_bytes / 4;
           int row = r_lo + rsub;
-          for (const int lim = min(r_end, tmin); row < lim; row += G, dst += dstep) {
+          for (const int lim = min(r_end, tmin); row < lim; row += RG, dst += dstep) {
             dst[0] = c0w; dst[1] = c1w; dst[2] = c2w;
           }
-          for (const int lim = min(r_end, tmax); row < lim; row += G, dst += dstep)
+          for (const int lim = min(r_end, tmax); row < lim; row += RG, dst += dstep)
             put_quad(dst, row < t0 ? C : w4.x, row < t1 ? C : w4.y, row < t2 ? C : w4.z,
                      row < t3 ? C : w4.w);
-          for (const int lim = min(r_end, bmin); row < lim; row += G, dst += dstep) {
+          for (const int lim = min(r_end, bmin); row < lim; row += RG, dst += dstep) {
             dst[0] = w0w; dst[1] = w1w; dst[2] = w2w;
           }
-          for (const int lim = min(r_end, bmax); row < lim; row += G, dst += dstep)
+          for (const int lim = min(r_end, bmax); row < lim; row += RG, dst += dstep)
             put_quad(dst, row < b0 ? w4.x : F, row < b1 ? w4.y : F, row < b2 ? w4.z : F,
                      row < b3 ? w4.w : F);
-          for (; row < r_end; row += G, dst += dstep) {
+          for (; row < r_end; row += RG, dst += dstep) {
             dst[0] = f0w; dst[1] = f1w; dst[2] = f2w;
           }
         }
       }
     } else {
       const int items = rows * W;
-      for (int p = lane; p < items; p += 32) {
+      for (int p = lane; p < items; p += G) {
         const int rr = p / W, c = p - rr * W;
         const uint32_t row = (uint32_t)(r_lo + rr);
         const uint32_t col = row < sm.t0(S)[c] ? C : (row < sm.b0(S)[c] ? sm.wrgb(S)[c] : F);
@@ -1166,31 +1221,31 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
       }
     }
     if (m > 0) {
-      __syncwarp();
-      draw_sprites<NC>(S, sm, m, band, r_lo, nullptr, 0, rows);
+      g.sync();
+      draw_sprites<NC, G>(S, sm, m, band, r_lo, nullptr, 0, rows);
     }
     // ship the band
     const int bytes = rows * row_bytes;
     uint8_t* gdst = frame + (size_t)r_lo * row_bytes;
     if (S.bulk) {
       bulk_fence();
-      __syncwarp();
+      g.sync();
       if (lane == 0) {
         bulk_store(gdst, band, (uint32_t)bytes);
         bulk_pending++;
       }
     } else {
-      __syncwarp();
-      for (int b = lane; b < bytes; b += 32) gdst[b] = band[b];
+      g.sync();
+      for (int b = lane; b < bytes; b += G) gdst[b] = band[b];
     }
   }
-  __syncwarp();
+  g.sync();
 }
 
 // Render one environment's frame (all 32 lanes of the warp participate).
 // Returns the status of the first failing column (or OK), warp-uniform.
 // _pycore.py:132-271.
-template <int NC>
+template <int NC, int G>
 __device__ __forceinline__ int render_env(const SpecDev& S, const uint32_t* __restrict__ cell,
                                           const uint32_t* __restrict__ solid, const WarpSmem& sm,
                                           const Env& e, uint8_t* __restrict__ frame,
@@ -1199,20 +1254,22 @@ __device__ __forceinline__ int render_env(const SpecDev& S, const uint32_t* __re
                                           unsigned long long* __restrict__ spritevis_out,
                                           int& bulk_pending, int& buf, const LaneGeo& lg,
                                           long long ti = 0) {
-  const int st = render_walls<NC>(S, cell, solid, sm, e, zbuf_out, rayinfo);
+  const int st = render_walls<NC, G>(S, cell, solid, sm, e, zbuf_out, rayinfo);
   if (st != TC_ST_OK) return st;
   TRACE(ti, 3);
-  const int m = render_sprites(S, sm, e, spritevis_out);
+  const int m = render_sprites<G>(S, sm, e, spritevis_out);
   TRACE(ti, 4);
-  render_frame_out<NC>(S, sm, m, frame, bulk_pending, buf, lg);
+  render_frame_out<NC, G>(S, sm, m, frame, bulk_pending, buf, lg);
   return TC_ST_OK;
 }
 
 // ------------------------------------------------------------- the kernels
 
+template <int G>
 __device__ __forceinline__ void load_env(const SpecDev& S, const StateDev& st, long long i,
                                          Env& e) {
-  const int lane = threadIdx.x & 31;
+  const Grp<G> g;
+  const int lane = g.lane;
   e.x = st.px[i]; e.y = st.py[i]; e.dx = st.dx[i]; e.dy = st.dy[i];
   e.health = st.health[i];
   e.inv = st.inv[i];
@@ -1221,17 +1278,25 @@ __device__ __forceinline__ void load_env(const SpecDev& S, const StateDev& st, l
   e.rctr = st.rctr[i];
   e.done = st.done[i];
   e.agoal = st.agoal[i];
-  const bool dop = lane < S.n_doors && st.dopen[i * S.n_doors + lane] != 0;
-  e.dmask = __ballot_sync(0xffffffffu, dop);
-  const bool a0 = lane < S.n_ent && st.ealive[i * S.n_ent + lane] != 0;
-  const bool a1 = lane + 32 < S.n_ent && st.ealive[i * S.n_ent + lane + 32] != 0;
-  e.emask = (unsigned long long)__ballot_sync(0xffffffffu, a0) |
-            ((unsigned long long)__ballot_sync(0xffffffffu, a1) << 32);
+  uint32_t dm = 0;
+  for (int b = 0; b < S.n_doors; b += G) {
+    const bool d = b + lane < S.n_doors && st.dopen[i * S.n_doors + b + lane] != 0;
+    dm |= g.ballot(d) << b;
+  }
+  e.dmask = dm;
+  unsigned long long em = 0;
+  for (int b = 0; b < S.n_ent; b += G) {
+    const bool a = b + lane < S.n_ent && st.ealive[i * S.n_ent + b + lane] != 0;
+    em |= (unsigned long long)g.ballot(a) << b;
+  }
+  e.emask = em;
 }
 
+template <int G>
 __device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, long long i,
                                           const Env& e) {
-  const int lane = threadIdx.x & 31;
+  const Grp<G> g;
+  const int lane = g.lane;
   if (lane == 0) {
     st.px[i] = e.x; st.py[i] = e.y; st.dx[i] = e.dx; st.dy[i] = e.dy;
     st.health[i] = e.health;
@@ -1241,10 +1306,10 @@ __device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, 
     st.done[i] = (uint8_t)e.done;
     st.agoal[i] = e.agoal;
   }
-  if (lane < S.n_doors) st.dopen[i * S.n_doors + lane] = (uint8_t)((e.dmask >> lane) & 1u);
-  if (lane < S.n_ent) st.ealive[i * S.n_ent + lane] = (uint8_t)((e.emask >> lane) & 1ULL);
-  if (lane + 32 < S.n_ent)
-    st.ealive[i * S.n_ent + lane + 32] = (uint8_t)((e.emask >> (lane + 32)) & 1ULL);
+  for (int d = lane; d < S.n_doors; d += G)
+    st.dopen[i * S.n_doors + d] = (uint8_t)((e.dmask >> d) & 1u);
+  for (int k = lane; k < S.n_ent; k += G)
+    st.ealive[i * S.n_ent + k] = (uint8_t)((e.emask >> k) & 1ULL);
 }
 
 // packed cells + stop codes into shared memory once per CTA
@@ -1267,30 +1332,36 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
 
 
 // MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387
-template <int NC>
+// MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387.
+// A group of G lanes owns one env at a time (G = 32: a warp; G = 16: each
+// half of a warp runs its own env).
+template <int NC, int G>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
 batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
              const long long* __restrict__ actions, const __grid_constant__ OutDev out,
              long long n, int mode, int auto_reset, int validate,
              tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NG = 32 / G;  // groups per warp
+  const Grp<G> g;
+  const int lane = g.lane;
+  const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;  // group id in the CTA
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
   const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
   const uint32_t *cell, *solid;
   stage_map(S, smap, cell, solid);
-  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem);
+  const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
-  const LaneGeo lg = lane_geo(S);
+  const LaneGeo lg = lane_geo<G>(S);
   int bulk_pending = 0, buf = 0;
   unsigned long long viol = 0;
   uint32_t badbits = 0;
-  // env scheduling: env i0 = global warp id first; envs beyond one wave are
+  // env scheduling: env i0 = global group id first; envs beyond one wave are
   // pulled dynamically from a device ticket counter (self-resetting: the
   // last CTA to finish zeroes it for the next launch)
-  const long long stride = (long long)gridDim.x * WARPS_PER_CTA;
+  const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
   const bool dyn = counters != nullptr && n > stride;
-  long long i = (long long)blockIdx.x * WARPS_PER_CTA + warp;
+  long long i = (long long)blockIdx.x * WARPS_PER_CTA * NG + grp;
   while (i < n) {
     // grab the next ticket now; its latency hides behind this env's work
     long long tnext = i + stride;
@@ -1302,9 +1373,9 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       e.rkey = st.rkey[i];
       e.rctr = st.rctr[i];
       reset_draws(S, e);
-      store_env(S, st, i, e);
+      store_env<G>(S, st, i, e);
     } else {
-      load_env(S, st, i, e);
+      load_env<G>(S, st, i, e);
       if (mode == MODE_STEP) {
         const long long act = actions[i];
         TRACE(i, 1);
@@ -1320,16 +1391,17 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
           }
           viol += (unsigned long long)o.violation;
           if (o.done && auto_reset) reset_draws(S, e);
-          store_env(S, st, i, e);
+          store_env<G>(S, st, i, e);
           TRACE(i, 2);
         }
       }
     }
     if (status == TC_ST_OK) {
-      status = render_env<NC>(S, cell, solid, sm, e, out.frames + (size_t)i * frame_bytes,
-                              out.zbuf ? out.zbuf + (size_t)i * S.obs_w : nullptr,
-                              out.rayinfo ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
-                              out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf, lg, i);
+      status = render_env<NC, G>(S, cell, solid, sm, e, out.frames + (size_t)i * frame_bytes,
+                                 out.zbuf ? out.zbuf + (size_t)i * S.obs_w : nullptr,
+                                 out.rayinfo ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
+                                 out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf,
+                                 lg, i);
     }
     if (lane == 0) out.statuses[i] = status;
     if (status != TC_ST_OK) badbits |= 1u << status;
@@ -1338,11 +1410,11 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       unsigned int smid;
       asm("mov.u32 %0, %smid;" : "=r"(smid));
       g_trace[i * 8 + 5] = gtime();
-      g_trace[i * 8 + 6] = smid | ((unsigned long long)warp << 16) |
+      g_trace[i * 8 + 6] = smid | ((unsigned long long)grp << 16) |
                            ((unsigned long long)blockIdx.x << 32);
     }
 #endif
-    i = dyn ? __shfl_sync(0xffffffffu, tnext, 0) : i + stride;
+    i = dyn ? g.shfl(tnext, 0) : i + stride;
   }
   if (lane == 0) {
     if (bulk_pending) bulk_wait_all();
@@ -1365,28 +1437,30 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
 
 // K fused steps with on-device policy actions (batch.py:141-153 draws) and
 // auto-reset; the env's state stays in registers across steps.
-template <int NC>
+template <int NC, int G>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
 rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
-               const __grid_constant__ OutDev out, long long n, const __grid_constant__ RolloutArgs ra,
-               tc_counters* __restrict__ counters) {
+               const __grid_constant__ OutDev out, long long n,
+               const __grid_constant__ RolloutArgs ra, tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NG = 32 / G;
+  const Grp<G> g;
+  const int lane = g.lane;
+  const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
   const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
   const uint32_t *cell, *solid;
   stage_map(S, smap, cell, solid);
-  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem);
+  const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
-  const LaneGeo lg = lane_geo(S);
+  const LaneGeo lg = lane_geo<G>(S);
   int bulk_pending = 0, buf = 0;
   uint32_t badbits = 0;
-
-  for (long long i = (long long)blockIdx.x * WARPS_PER_CTA + warp; i < n;
-       i += (long long)gridDim.x * WARPS_PER_CTA) {
+  const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
+  for (long long i = (long long)blockIdx.x * WARPS_PER_CTA * NG + grp; i < n; i += stride) {
     Env e;
     int st_acc = TC_ST_OK;
-    load_env(S, st, i, e);
+    load_env<G>(S, st, i, e);
     int ring_k = 0;
     for (int k = 0; k < ra.k_steps; k++) {
       const long long step = ra.step0 + k;
@@ -1403,85 +1477,15 @@ rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateD
       if (o.done) reset_draws(S, e);
       const size_t slot = (size_t)ring_k * (size_t)n + (size_t)i;
       if (++ring_k == ra.frame_ring) ring_k = 0;
-      const int status = render_env<NC>(S, cell, solid, sm, e, out.frames + slot * frame_bytes,
-                                        nullptr, nullptr, nullptr, bulk_pending, buf, lg);
+      const int status = render_env<NC, G>(S, cell, solid, sm, e, out.frames + slot * frame_bytes,
+                                           nullptr, nullptr, nullptr, bulk_pending, buf, lg);
       if (status != TC_ST_OK) {
         badbits |= 1u << status;
         if (st_acc == TC_ST_OK) st_acc = status;
       }
     }
-    store_env(S, st, i, e);
+    store_env<G>(S, st, i, e);
     if (lane == 0 && out.statuses) out.statuses[i] = st_acc;
-  }
-  if (lane == 0) {
-    if (bulk_pending) bulk_wait_all();
-    if (counters && badbits) atomicOr(&counters->bad_status, badbits);
-  }
-}
-
-// Phase-synchronised rollout: the CTA's warps run each step's phases
-// (dynamics | walls | sprites | frame) in lockstep with CTA barriers, so at
-// any moment the SM executes one phase's code (the fused step's full code
-// footprint exceeds the instruction cache; one phase's does not).
-template <int NC, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 3 : 1))
-rollout_phased_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
-                      const __grid_constant__ OutDev out, long long n, const __grid_constant__ RolloutArgs ra,
-                      tc_counters* __restrict__ counters) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
-  const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
-  const uint32_t *cell, *solid;
-  stage_map(S, smap, cell, solid);
-  const WarpSmem sm = carve(smem + map_bytes + warp * S.warp_smem);
-  const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
-  const LaneGeo lg = lane_geo(S);
-  int bulk_pending = 0, buf = 0;
-  uint32_t badbits = 0;
-  for (long long base = (long long)blockIdx.x * WARPS; base < n;
-       base += (long long)gridDim.x * WARPS) {
-    const long long i = base + warp;
-    const bool active = i < n;
-    Env e;
-    int st_acc = TC_ST_OK;
-    if (active) load_env(S, st, i, e);
-    int ring_k = 0;
-    for (int k = 0; k < ra.k_steps; k++) {
-      int status = TC_ST_OK, m = 0;
-      size_t slot = 0;
-      if (active) {
-        const long long step = ra.step0 + k;
-        unsigned long long ctr = (unsigned long long)(step * ra.n_total + ra.base + i);
-        const int act = ra.tags[draw_below(ra.policy_key, ctr, (uint64_t)ra.n_tags)];
-        const StepOut o = step_dynamics(S, cell, solid, e, act, 0);
-        const size_t kn = (size_t)k * (size_t)n + (size_t)i;
-        if (lane == 0) {
-          if (out.rewards) out.rewards[kn] = o.reward;
-          if (out.dones) out.dones[kn] = (uint8_t)o.done;
-          if (out.truncs) out.truncs[kn] = (uint8_t)o.trunc;
-          if (out.events) out.events[kn] = o.events;
-        }
-        if (o.done) reset_draws(S, e);
-        slot = (size_t)ring_k * (size_t)n + (size_t)i;
-      }
-      if (++ring_k == ra.frame_ring) ring_k = 0;
-      __syncthreads();
-      if (active) status = render_walls<NC>(S, cell, solid, sm, e, nullptr, nullptr);
-      __syncthreads();
-      if (active && status == TC_ST_OK) m = render_sprites(S, sm, e, nullptr);
-      __syncthreads();
-      if (active && status == TC_ST_OK)
-        render_frame_out<NC>(S, sm, m, out.frames + slot * frame_bytes, bulk_pending, buf, lg);
-      if (status != TC_ST_OK) {
-        badbits |= 1u << status;
-        if (st_acc == TC_ST_OK) st_acc = status;
-      }
-    }
-    if (active) {
-      store_env(S, st, i, e);
-      if (lane == 0 && out.statuses) out.statuses[i] = st_acc;
-    }
   }
   if (lane == 0) {
     if (bulk_pending) bulk_wait_all();
@@ -1521,9 +1525,6 @@ __global__ void cast_ray_kernel(const uint32_t* cell, int h, int w, uint32_t dma
 // =================================================================== host
 struct tc_spec {
   SpecDev dev;
-  int phased = 0;        // TILECAST_PHASED=<warps>: phase-synchronised rollout
-  int phased_ctas = 0;
-  size_t phased_smem = 0;
   void* blob = nullptr;
   int nc = 1;
   int max_ctas = 0;  // grid size for one full wave
@@ -1550,60 +1551,56 @@ uint32_t pack_rgb(const uint8_t* p) {
   return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16);
 }
 
-int pick_nc(int obs_w) {
-  const int need = (obs_w + 31) / 32;
+// columns per lane for a group of G lanes, rounded to an instantiated NC
+int pick_nc(int obs_w, int group) {
+  const int need = (obs_w + group - 1) / group;
   const int opts[] = {1, 2, 3, 4, 8, 16, 32};
   for (int o : opts)
     if (o >= need) return o;
   return 32;
 }
 
-template <int NC>
-const void* batch_fn() { return (const void*)batch_kernel<NC>; }
-template <int NC>
-const void* rollout_fn() { return (const void*)rollout_kernel<NC>; }
+template <int NC, int G>
+const void* batch_fn() { return (const void*)batch_kernel<NC, G>; }
+template <int NC, int G>
+const void* rollout_fn() { return (const void*)rollout_kernel<NC, G>; }
 
-const void* select_batch(int nc) {
-  switch (nc) {
-    case 1: return batch_fn<1>();
-    case 2: return batch_fn<2>();
-    case 3: return batch_fn<3>();
-    case 4: return batch_fn<4>();
-    case 8: return batch_fn<8>();
-    case 16: return batch_fn<16>();
-    default: return batch_fn<32>();
-  }
-}
-template <int NC, int WP>
-const void* phased_fn() { return (const void*)rollout_phased_kernel<NC, WP>; }
-const void* select_phased(int nc, int wp) {
-  if (wp == 8) {
+const void* select_batch(int nc, int group) {
+  if (group == 16) {
     switch (nc) {
-      case 1: return phased_fn<1, 8>();
-      case 2: return phased_fn<2, 8>();
-      case 4: return phased_fn<4, 8>();
-      default: return nullptr;
+      case 1: return batch_fn<1, 16>();
+      case 2: return batch_fn<2, 16>();
+      case 3: return batch_fn<3, 16>();
+      default: return batch_fn<4, 16>();
     }
   }
-  if (wp == 16) {
+  switch (nc) {
+    case 1: return batch_fn<1, 32>();
+    case 2: return batch_fn<2, 32>();
+    case 3: return batch_fn<3, 32>();
+    case 4: return batch_fn<4, 32>();
+    case 8: return batch_fn<8, 32>();
+    case 16: return batch_fn<16, 32>();
+    default: return batch_fn<32, 32>();
+  }
+}
+const void* select_rollout(int nc, int group) {
+  if (group == 16) {
     switch (nc) {
-      case 1: return phased_fn<1, 16>();
-      case 2: return phased_fn<2, 16>();
-      case 4: return phased_fn<4, 16>();
-      default: return nullptr;
+      case 1: return rollout_fn<1, 16>();
+      case 2: return rollout_fn<2, 16>();
+      case 3: return rollout_fn<3, 16>();
+      default: return rollout_fn<4, 16>();
     }
   }
-  return nullptr;
-}
-const void* select_rollout(int nc) {
   switch (nc) {
-    case 1: return rollout_fn<1>();
-    case 2: return rollout_fn<2>();
-    case 3: return rollout_fn<3>();
-    case 4: return rollout_fn<4>();
-    case 8: return rollout_fn<8>();
-    case 16: return rollout_fn<16>();
-    default: return rollout_fn<32>();
+    case 1: return rollout_fn<1, 32>();
+    case 2: return rollout_fn<2, 32>();
+    case 3: return rollout_fn<3, 32>();
+    case 4: return rollout_fn<4, 32>();
+    case 8: return rollout_fn<8, 32>();
+    case 16: return rollout_fn<16, 32>();
+    default: return rollout_fn<32, 32>();
   }
 }
 
@@ -1691,19 +1688,34 @@ int launch_geometry(tc_spec* s) {
   d.bulk = (row_bytes % 16) == 0;
   d.mirror = (d.obs_h % 2 == 0 && d.obs_h <= 254 && d.obs_w % 16 == 0 && d.bulk) ? 1 : 0;
   d.mir_rpi = (d.obs_w / 16) >= 32 ? 1 : 32 / (d.obs_w / 16 > 0 ? d.obs_w / 16 : 1);
+  d.mir_rpi16 = (d.obs_w / 16) >= 16 ? 1 : 16 / (d.obs_w / 16 > 0 ? d.obs_w / 16 : 1);
   int rows = (d.mirror ? BAND_BYTES_TARGET / 2 : BAND_BYTES_TARGET) / row_bytes;
   if (rows < 1) rows = 1;
   if (rows > d.obs_h) rows = d.obs_h;
   d.band_rows = rows;
   d.band_stride = align16(rows * row_bytes);
+  // lanes per env: two envs per warp (16 lanes each) for obs_w <= 64, where
+  // 16 lanes x 4 columns still cover a row (fits every env of a 4096-env
+  // batch on the GPU at once); TILECAST_GROUP overrides (experiments)
+  const char* gr = getenv("TILECAST_GROUP");
+  d.group = gr ? atoi(gr) : (d.obs_w <= 64 ? 16 : 32);
+  if (d.group != 16 || d.obs_w > 64) d.group = 32;
+  // frame store path: 0 = staged bands + TMA bulk stores, 1 = 16-byte stores
+  // straight from registers (no staging smem -> more resident envs), 2 =
+  // staged bands + coalesced LDS/STG. Measured best: 1 with 16-lane groups,
+  // 0 with full warps; TILECAST_DIRECT overrides.
   const char* dr = getenv("TILECAST_DIRECT");
-  d.direct = (dr && atoi(dr) && d.mirror) ? 1 : 0;
-  d.warp_smem = warp_smem_layout(d, d.direct ? 0 : (d.mirror ? 4 : 2));
+  d.direct = d.mirror ? (dr ? atoi(dr) : (d.group == 16 ? 1 : 0)) : 0;
+  const char* np = getenv("TILECAST_NPAIRS");
+  d.npairs = np ? atoi(np) : 2;
+  if (d.npairs < 2) d.npairs = 2;
+  if (d.npairs > 4) d.npairs = 4;
+  d.warp_smem = warp_smem_layout(d, d.direct == 1 ? 0 : (d.mirror ? 2 * d.npairs : 2));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
   const size_t map_bytes = d.smem_map ? (size_t)align16(d.h * d.w * 8) : 0;
-  s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * d.warp_smem;
-  s->nc = pick_nc(d.obs_w);
-  const void* fns[2] = {select_batch(s->nc), select_rollout(s->nc)};
+  s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * (32 / d.group) * d.warp_smem;
+  s->nc = pick_nc(d.obs_w, d.group);
+  const void* fns[2] = {select_batch(s->nc, d.group), select_rollout(s->nc, d.group)};
   // the attribute is per function, shared by every spec: raise it to the
   // device's opt-in maximum once instead of per spec (occupancy follows the
   // smem each launch actually asks for)
@@ -1719,20 +1731,6 @@ int launch_geometry(tc_spec* s) {
                                                         s->smem_bytes));
   if (per_sm < 1) return fail(TC_E_CAPACITY, "kernel does not fit on an SM");
   s->max_ctas = per_sm * device_sm_count();
-  const char* ph = getenv("TILECAST_PHASED");
-  s->phased = ph ? atoi(ph) : 0;
-  if (s->phased && select_phased(s->nc, s->phased)) {
-    const void* fn = select_phased(s->nc, s->phased);
-    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    s->phased_smem = map_bytes + (size_t)s->phased * d.warp_smem;
-    int pc = 0;
-    TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pc, fn, s->phased * 32,
-                                                          s->phased_smem));
-    s->phased_ctas = pc * device_sm_count();
-    if (pc < 1) s->phased = 0;
-  } else {
-    s->phased = 0;
-  }
   return TC_OK;
 }
 
@@ -1757,7 +1755,8 @@ OutDev to_dev(const tc_out* o) {
 }
 
 int grid_for(const tc_spec* s, int64_t n) {
-  const int64_t want = (n + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  const int per_cta = WARPS_PER_CTA * (32 / s->dev.group);  // envs per CTA pass
+  const int64_t want = (n + per_cta - 1) / per_cta;
   return (int)(want < s->max_ctas ? want : s->max_ctas);
 }
 
@@ -1889,7 +1888,7 @@ int tc_batch_kernel(const tc_spec* s, const tc_state* state, const int64_t* acti
   int m = mode, ar = auto_reset, va = validate;
   SpecDev spec = d;
   void* args[] = {&spec, &sd, &acts, &od, (void*)&nn, &m, &ar, &va, &counters_dev};
-  TC_CUDA(cudaLaunchKernel(select_batch(s->nc), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
+  TC_CUDA(cudaLaunchKernel(select_batch(s->nc, s->dev.group), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
                            s->smem_bytes, (cudaStream_t)stream));
   return TC_OK;
 }
@@ -1918,15 +1917,8 @@ int tc_rollout(const tc_spec* s, const tc_state* state, const tc_out* out, int64
   const long long nn = n;
   SpecDev spec = s->dev;
   void* args[] = {&spec, &sd, &od, (void*)&nn, &ra, &counters_dev};
-  if (s->phased) {
-    const int64_t want = (n + s->phased - 1) / s->phased;
-    const int g = (int)(want < s->phased_ctas ? want : s->phased_ctas);
-    TC_CUDA(cudaLaunchKernel(select_phased(s->nc, s->phased), dim3(g), dim3(s->phased * 32),
-                             args, s->phased_smem, (cudaStream_t)stream));
-    return TC_OK;
-  }
   const int grid = grid_for(s, n);
-  TC_CUDA(cudaLaunchKernel(select_rollout(s->nc), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
+  TC_CUDA(cudaLaunchKernel(select_rollout(s->nc, s->dev.group), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
                            s->smem_bytes, (cudaStream_t)stream));
   return TC_OK;
 }
