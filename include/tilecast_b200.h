@@ -157,6 +157,15 @@ int tc_batch_kernel(const tc_spec *spec, const tc_state *state,
                     int32_t mode, int32_t auto_reset, int32_t validate,
                     tc_counters *counters_dev, void *stream);
 
+/* Out-of-place step: reads state_in, writes the stepped state to state_out
+ * (both DEVICE pointers, may not overlap unless equal). This is batch_step's
+ * "new BatchState from the old one" (batch.py:109-138) without the
+ * reference's 13 per-step state copies (tables.py:217-220). */
+int tc_batch_step_into(const tc_spec *spec, const tc_state *state_in,
+                       const tc_state *state_out, const int64_t *actions_dev,
+                       const tc_out *out, int64_t n, int32_t auto_reset,
+                       int32_t validate, tc_counters *counters_dev, void *stream);
+
 /* K fused steps in one launch with on-device uniform-random actions drawn
  * exactly as batch.policy_actions (batch.py:141-153) would draw them for
  * steps [step0, step0+K) of an (n_total)-env rollout whose env 0 is global

@@ -35,7 +35,8 @@ from . import layout as L
 from . import rng
 from .dynamics import ACTION_NAMES, Action, EnvState, state_from_arrays
 from .engine import (DeviceOut, DeviceSpec, DeviceState, device_spec, launch_batch,
-                     new_counters, read_counters, resolve_device, stream_ptr)
+                     launch_step_into, new_counters, read_counters, resolve_device,
+                     stream_ptr)
 from .geometry import ContractError
 from .suite import EnvSpec
 
@@ -176,11 +177,17 @@ def _coerce_actions(bs: BatchState, actions) -> torch.Tensor:
 
 
 def batch_step(bs: BatchState, actions: Sequence[Action | int] | np.ndarray | torch.Tensor, *,
-               validate: bool = False, reuse: bool = False,
-               sync_checks: bool = False) -> tuple[BatchState, torch.Tensor, torch.Tensor]:
+               validate: bool = False, reuse: bool = False, sync_checks: bool = False,
+               copy_outputs: bool = True) -> tuple[BatchState, torch.Tensor, torch.Tensor]:
     """Step every env once; finished episodes auto-reset in the same launch
     (their frame shows the new episode; the terminal reward / done flag are
-    still reported). Returns (next_state, rewards, dones) as device tensors."""
+    still reported). Returns (next_state, rewards, dones) as device tensors.
+
+    The step is out-of-place (the old BatchState stays valid, batch.py:31-34)
+    but needs no state copy: the kernel reads the old blocks and writes the
+    new ones. With ``copy_outputs=False`` rewards / dones are views of the
+    successor's output block (valid until that block is recycled by a later
+    ``reuse=True`` step) -- one launch per step, nothing else."""
     spec, t = bs.spec, bs.spec.tables
     acts = _coerce_actions(bs, actions)
     if reuse and bs._retired:
@@ -189,15 +196,37 @@ def batch_step(bs: BatchState, actions: Sequence[Action | int] | np.ndarray | to
         sb = DeviceState.alloc(bs.n, t.n_doors, t.n_entities, bs.device)
         ob = DeviceOut.alloc(bs.n, t.obs_height, t.obs_width, bs.device,
                              debug=bs._ob.zbuf is not None)
-    sb.copy_from(bs._sb)
-    launch_batch(bs._ds, sb, acts, ob, bs.n, L.MODE_STEP, True, validate, bs._counters)
+    launch_step_into(bs._ds, bs._sb, sb, acts, ob, bs.n, True, validate, bs._counters)
     new = BatchState(spec=spec, n=bs.n, _ds=bs._ds, _sb=sb, _ob=ob, _counters=bs._counters,
                      base=bs.base, n_total=bs.n_total,
                      _retired=(bs._sb, bs._ob) if reuse else (),
                      _stage=bs._stage)
     if validate or sync_checks:
         new.check()
-    return new, ob.rewards, ob.dones != 0
+    rewards, dones = ob.rewards, ob.dones.view(torch.bool)
+    if copy_outputs:
+        rewards, dones = rewards.clone(), dones.clone()
+    return new, rewards, dones
+
+
+_pinned_cache: dict = {}
+
+
+def to_host(*tensors: torch.Tensor) -> tuple[np.ndarray, ...]:
+    """Copy device tensors to host numpy arrays with async copies into pinned
+    buffers and ONE stream synchronisation (instead of one sync per .cpu())."""
+    outs = []
+    dev = tensors[0].device
+    for k, x in enumerate(tensors):
+        key = (k, x.dtype, tuple(x.shape))
+        buf = _pinned_cache.get(key)
+        if buf is None:
+            buf = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+            _pinned_cache[key] = buf
+        buf.copy_(x, non_blocking=True)
+        outs.append(buf)
+    torch.cuda.current_stream(dev).synchronize()
+    return tuple(b.numpy().copy() for b in outs)
 
 
 def batch_step_inplace(bs: BatchState, actions: torch.Tensor) -> BatchState:

@@ -1302,6 +1302,7 @@ __device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, 
     st.health[i] = e.health;
     st.inv[i] = (uint8_t)e.inv;
     st.t[i] = e.t;
+    st.rkey[i] = e.rkey;
     st.rctr[i] = e.rctr;
     st.done[i] = (uint8_t)e.done;
     st.agoal[i] = e.agoal;
@@ -1338,7 +1339,8 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
 template <int NC, int G>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
 batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
-             const long long* __restrict__ actions, const __grid_constant__ OutDev out,
+             const __grid_constant__ StateDev so, const long long* __restrict__ actions,
+             const __grid_constant__ OutDev out,
              long long n, int mode, int auto_reset, int validate,
              tc_counters* __restrict__ counters) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1373,7 +1375,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       e.rkey = st.rkey[i];
       e.rctr = st.rctr[i];
       reset_draws(S, e);
-      store_env<G>(S, st, i, e);
+      store_env<G>(S, so, i, e);
     } else {
       load_env<G>(S, st, i, e);
       if (mode == MODE_STEP) {
@@ -1381,6 +1383,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
         TRACE(i, 1);
         if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
           status = TC_ST_BAD_ACTION;
+          store_env<G>(S, so, i, e);  // out-of-place: carry the state over
         } else {
           const StepOut o = step_dynamics(S, cell, solid, e, (int)act, validate);
           if (lane == 0) {
@@ -1391,7 +1394,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
           }
           viol += (unsigned long long)o.violation;
           if (o.done && auto_reset) reset_draws(S, e);
-          store_env<G>(S, st, i, e);
+          store_env<G>(S, so, i, e);
           TRACE(i, 2);
         }
       }
@@ -1865,9 +1868,10 @@ int tc_spec_destroy(tc_spec* s) {
   return e == cudaSuccess ? TC_OK : cuda_fail(e, "cudaFree(spec)");
 }
 
-int tc_batch_kernel(const tc_spec* s, const tc_state* state, const int64_t* actions_dev,
-                    const tc_out* out, int64_t n, int32_t mode, int32_t auto_reset,
-                    int32_t validate, tc_counters* counters_dev, void* stream) {
+static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc_state* state_out,
+                               const int64_t* actions_dev, const tc_out* out, int64_t n,
+                               int32_t mode, int32_t auto_reset, int32_t validate,
+                               tc_counters* counters_dev, void* stream) {
   if (!s || !state || !out) return fail(TC_E_INVALID, "NULL spec/state/out");
   if (n < 0) return fail(TC_E_INVALID, "n must be >= 0");
   if (mode != TC_MODE_RESET && mode != TC_MODE_STEP && mode != MODE_RENDER)
@@ -1881,16 +1885,33 @@ int tc_batch_kernel(const tc_spec* s, const tc_state* state, const int64_t* acti
   if (d.bulk && (reinterpret_cast<uintptr_t>(out->frames) & 15u))
     return fail(TC_E_INVALID, "frames must be 16-byte aligned");
   StateDev sd = to_dev(state);
+  StateDev so = to_dev(state_out ? state_out : state);
   OutDev od = to_dev(out);
   const int grid = grid_for(s, n);
   const long long nn = n;
   const long long* acts = reinterpret_cast<const long long*>(actions_dev);
   int m = mode, ar = auto_reset, va = validate;
   SpecDev spec = d;
-  void* args[] = {&spec, &sd, &acts, &od, (void*)&nn, &m, &ar, &va, &counters_dev};
-  TC_CUDA(cudaLaunchKernel(select_batch(s->nc, s->dev.group), dim3(grid), dim3(WARPS_PER_CTA * 32), args,
-                           s->smem_bytes, (cudaStream_t)stream));
+  void* args[] = {&spec, &sd, &so, &acts, &od, (void*)&nn, &m, &ar, &va, &counters_dev};
+  TC_CUDA(cudaLaunchKernel(select_batch(s->nc, s->dev.group), dim3(grid),
+                           dim3(WARPS_PER_CTA * 32), args, s->smem_bytes, (cudaStream_t)stream));
   return TC_OK;
+}
+
+int tc_batch_kernel(const tc_spec* s, const tc_state* state, const int64_t* actions_dev,
+                    const tc_out* out, int64_t n, int32_t mode, int32_t auto_reset,
+                    int32_t validate, tc_counters* counters_dev, void* stream) {
+  return launch_batch_kernel(s, state, nullptr, actions_dev, out, n, mode, auto_reset, validate,
+                             counters_dev, stream);
+}
+
+int tc_batch_step_into(const tc_spec* s, const tc_state* state_in, const tc_state* state_out,
+                       const int64_t* actions_dev, const tc_out* out, int64_t n,
+                       int32_t auto_reset, int32_t validate, tc_counters* counters_dev,
+                       void* stream) {
+  if (!state_out) return fail(TC_E_INVALID, "state_out is NULL");
+  return launch_batch_kernel(s, state_in, state_out, actions_dev, out, n, TC_MODE_STEP,
+                             auto_reset, validate, counters_dev, stream);
 }
 
 int tc_rollout(const tc_spec* s, const tc_state* state, const tc_out* out, int64_t n,

@@ -121,7 +121,12 @@ class DeviceState:
         return out
 
     def c_struct(self) -> N.TcState:
-        return N.state_struct(self.tensors())
+        # the tensors of a block never change identity: build the struct once
+        c = self.__dict__.get("_c")
+        if c is None:
+            c = N.state_struct(self.tensors())
+            self.__dict__["_c"] = c
+        return c
 
 
 @dataclass
@@ -157,7 +162,11 @@ class DeviceOut:
         return {f.name: getattr(self, f.name) for f in fields(self)}
 
     def c_struct(self) -> N.TcOut:
-        return N.out_struct(self.tensors())
+        c = self.__dict__.get("_c")
+        if c is None:
+            c = N.out_struct(self.tensors())
+            self.__dict__["_c"] = c
+        return c
 
 
 def new_counters(device) -> torch.Tensor:
@@ -168,6 +177,17 @@ def new_counters(device) -> torch.Tensor:
 def read_counters(c: torch.Tensor) -> tuple[int, int]:
     v = c.cpu().numpy()
     return int(v[0]), int(v[1]) & 0xFFFFFFFF
+
+
+def launch_step_into(ds: DeviceSpec, st_in: DeviceState, st_out: DeviceState,
+                     actions: torch.Tensor, out: DeviceOut, n: int, auto_reset: bool,
+                     validate: bool, counters: torch.Tensor | None) -> None:
+    """One fused step reading st_in and writing st_out (tc_batch_step_into)."""
+    with torch.cuda.device(ds.device):
+        N.check(N.lib().tc_batch_step_into(
+            ds.handle, N.C.byref(st_in.c_struct()), N.C.byref(st_out.c_struct()),
+            N.ptr(actions), N.C.byref(out.c_struct()), n, 1 if auto_reset else 0,
+            1 if validate else 0, N.ptr(counters), stream_ptr(ds.device)), "tc_batch_step_into")
 
 
 def launch_batch(ds: DeviceSpec, st: DeviceState, actions: torch.Tensor | None,
