@@ -262,10 +262,18 @@ def main():
     from paper_2605_19926_b200 import layout as L
     from paper_2605_19926_b200.engine import DeviceOut, launch_batch
 
+    # one process per GPU; TILECAST_DIST_BACKEND=gloo lets a test run several
+    # ranks on fewer GPUs (independent kernels, reductions on CPU tensors)
+    backend = os.environ.get("TILECAST_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    rdev = dev if backend == "nccl" else torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2605_19926_b200.shard import reduce_episode_stats, shard_range
 
@@ -323,7 +331,7 @@ def main():
     elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = [elapsed_ms / args.steps]  # per-launch average over the graph replay
     if world > 1:
-        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
     bs.check()
@@ -341,7 +349,7 @@ def main():
     torch.cuda.synchronize(dev)
     rollout_ms = r0.elapsed_time(r1)
     if world > 1:
-        t = torch.tensor([rollout_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([rollout_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         rollout_ms = float(t.item())
     rollout_value = n_total * args.steps / (rollout_ms / 1e3)
@@ -366,9 +374,9 @@ def main():
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
     stats = reduce_episode_stats({"reward_sum": rsum, "env_steps": n * args.e2e_steps},
-                                 device=dev)  # the optional NCCL stats reduction
+                                 device=rdev)  # the optional NCCL stats reduction
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = n_total * args.e2e_steps / e2e_s

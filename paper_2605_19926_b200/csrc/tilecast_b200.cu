@@ -60,6 +60,9 @@ constexpr int WARPS_PER_CTA = 4;
 #ifndef TC_TRACE
 #define TC_TRACE 0  // perf experiments only: per-env phase timestamps
 #endif
+#ifndef TC_STORE
+#define TC_STORE __stcs  // frame stores (direct path): streaming / evict-first
+#endif
 #ifndef TC_MIN_CTAS
 #define TC_MIN_CTAS 5  // resident CTAs per SM the register budget is sized for
 #endif
@@ -1119,12 +1122,12 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
         }
         uint4* dt = reinterpret_cast<uint4*>(top);
         uint4* db = reinterpret_cast<uint4*>(bot);
-        __stcs(dt + 0, make_uint4(tw[0], tw[1], tw[2], tw[3]));
-        __stcs(dt + 1, make_uint4(tw[4], tw[5], tw[6], tw[7]));
-        __stcs(dt + 2, make_uint4(tw[8], tw[9], tw[10], tw[11]));
-        __stcs(db + 0, make_uint4(bw[0], bw[1], bw[2], bw[3]));
-        __stcs(db + 1, make_uint4(bw[4], bw[5], bw[6], bw[7]));
-        __stcs(db + 2, make_uint4(bw[8], bw[9], bw[10], bw[11]));
+        TC_STORE(dt + 0, make_uint4(tw[0], tw[1], tw[2], tw[3]));
+        TC_STORE(dt + 1, make_uint4(tw[4], tw[5], tw[6], tw[7]));
+        TC_STORE(dt + 2, make_uint4(tw[8], tw[9], tw[10], tw[11]));
+        TC_STORE(db + 0, make_uint4(bw[0], bw[1], bw[2], bw[3]));
+        TC_STORE(db + 1, make_uint4(bw[4], bw[5], bw[6], bw[7]));
+        TC_STORE(db + 2, make_uint4(bw[8], bw[9], bw[10], bw[11]));
       }
     }
   }
@@ -1692,7 +1695,9 @@ int launch_geometry(tc_spec* s) {
   d.mirror = (d.obs_h % 2 == 0 && d.obs_h <= 254 && d.obs_w % 16 == 0 && d.bulk) ? 1 : 0;
   d.mir_rpi = (d.obs_w / 16) >= 32 ? 1 : 32 / (d.obs_w / 16 > 0 ? d.obs_w / 16 : 1);
   d.mir_rpi16 = (d.obs_w / 16) >= 16 ? 1 : 16 / (d.obs_w / 16 > 0 ? d.obs_w / 16 : 1);
-  int rows = (d.mirror ? BAND_BYTES_TARGET / 2 : BAND_BYTES_TARGET) / row_bytes;
+  const char* bb = getenv("TILECAST_BAND_BYTES");
+  const int band_target = bb ? atoi(bb) : (d.mirror ? BAND_BYTES_TARGET / 2 : BAND_BYTES_TARGET);
+  int rows = band_target / row_bytes;
   if (rows < 1) rows = 1;
   if (rows > d.obs_h) rows = d.obs_h;
   d.band_rows = rows;
