@@ -360,16 +360,14 @@ def main():
     host_acts = tc.policy_actions(spec, n_total, args.e2e_steps + 3, seed + 1)[:, base:base + n]
     eb = tc.batch_reset(spec, n, seed + 1, device=dev, base=base, n_total=n_total)
     for s in range(3):
-        eb, r, d = tc.batch_step(eb, host_acts[s], reuse=True, copy_outputs=False)
-        tc.to_host(r, d)
+        eb, rh, dh = tc.batch_step_host(eb, host_acts[s], reuse=True)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     rsum = 0.0
     for s in range(args.e2e_steps):
-        eb, r, d = tc.batch_step(eb, host_acts[3 + s], reuse=True, copy_outputs=False)
-        rh, dh = tc.to_host(r, d)
+        eb, rh, dh = tc.batch_step_host(eb, host_acts[3 + s], reuse=True)
         rsum += float(rh.sum())
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
@@ -408,8 +406,8 @@ def main():
                              f"({ring * frame_bytes / 2**20:.0f} MiB > 2x L2)"},
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 9,
-                    "api": "batch_step(host numpy actions, reuse=True, copy_outputs=False)"
-                           " + to_host(rewards, dones) every step",
+                    "api": "batch_step_host(numpy actions, reuse=True) -> numpy rewards,"
+                           " dones (H2D + fused step + D2H + sync per step)",
                     "episode_stats": stats},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

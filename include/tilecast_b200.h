@@ -166,6 +166,18 @@ int tc_batch_step_into(const tc_spec *spec, const tc_state *state_in,
                        const tc_out *out, int64_t n, int32_t auto_reset,
                        int32_t validate, tc_counters *counters_dev, void *stream);
 
+/* batch_step over HOST buffers in one call (batch.py:109-138 semantics, the
+ * reference's numpy-in / numpy-out contract): H2D of actions_host into
+ * actions_dev, one fused out-of-place step, D2H of rewards (f64[n]) and
+ * dones (u8[n]) into host memory, stream synchronised on return. Any host
+ * pointer may be pageable; rewards_host / dones_host may be NULL. */
+int tc_batch_step_host(const tc_spec *spec, const tc_state *state_in,
+                       const tc_state *state_out, const int64_t *actions_host,
+                       int64_t *actions_dev, const tc_out *out, int64_t n,
+                       int32_t auto_reset, int32_t validate,
+                       tc_counters *counters_dev, double *rewards_host,
+                       uint8_t *dones_host, void *stream);
+
 /* K fused steps in one launch with on-device uniform-random actions drawn
  * exactly as batch.policy_actions (batch.py:141-153) would draw them for
  * steps [step0, step0+K) of an (n_total)-env rollout whose env 0 is global

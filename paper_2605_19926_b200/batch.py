@@ -121,12 +121,29 @@ class _ActionStage:
         self.dev = [torch.empty(n, dtype=torch.int64, device=device) for _ in range(2)]
         self.events = [torch.cuda.Event() for _ in range(2)]
         self.k = 0
+        self.np = [p.numpy() for p in self.pinned]
+        # batch_step_host's synchronous staging (actions in, rewards / dones out)
+        # results land as [rewards f64[n] | dones u8[n]], one D2H copy
+        self._h_act = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        self._h_res = torch.empty(9 * n, dtype=torch.uint8, pin_memory=True)
+        self.h_act = self._h_act.numpy()
+        res = self._h_res.numpy()
+        self.h_rew = res[:8 * n].view(np.float64)
+        self.h_done = res[8 * n:].view(np.bool_)
+        self.h_act_ptr = self._h_act.data_ptr()
+        self.h_rew_ptr = self._h_res.data_ptr()
+        self.h_done_ptr = self.h_rew_ptr + 8 * n
+        self.dev_ptr = self.dev[0].data_ptr()
+        self.calls: dict = {}
 
-    def put(self, acts: np.ndarray) -> torch.Tensor:
+    def next_buffer(self) -> np.ndarray:
+        """The next pinned buffer, once the H2D copy that last read it is done."""
         self.k ^= 1
+        self.events[self.k].synchronize()
+        return self.np[self.k]
+
+    def upload(self) -> torch.Tensor:
         k = self.k
-        self.events[k].synchronize()
-        self.pinned[k].numpy()[:] = acts
         self.dev[k].copy_(self.pinned[k], non_blocking=True)
         self.events[k].record(torch.cuda.current_stream(self.dev[k].device))
         return self.dev[k]
@@ -158,22 +175,95 @@ def _coerce_actions(bs: BatchState, actions) -> torch.Tensor:
         if actions.shape != (bs.n,):
             raise ContractError(f"actions must have shape ({bs.n},), got {tuple(actions.shape)}")
         return actions.to(torch.int64).contiguous()
-    acts = np.asarray(actions.cpu() if isinstance(actions, torch.Tensor) else actions,
-                      dtype=np.int64)
-    if acts.shape != (bs.n,):
-        raise ContractError(f"actions must have shape ({bs.n},), got {acts.shape}")
-    if acts.min(initial=0) < 0 or acts.max(initial=0) >= L.A_COUNT:
+    if bs._stage is None:
+        bs._stage = _ActionStage(bs.n, bs.device)
+    host = actions.cpu().numpy() if isinstance(actions, torch.Tensor) else actions
+    if not isinstance(host, np.ndarray):
+        host = np.asarray(host, dtype=np.int64)
+    if host.shape != (bs.n,):
+        raise ContractError(f"actions must have shape ({bs.n},), got {host.shape}")
+    buf = bs._stage.next_buffer()            # pinned int64[n]; one conversion pass
+    np.copyto(buf, host, casting="unsafe")
+    if (buf.view(np.uint64) >= L.A_COUNT).any():  # negatives wrap to huge
         raise ContractError(f"action tags must be in [0, {L.A_COUNT})")
     legal = bs.spec.tables.legal
-    ok = legal[acts] != 0
-    if not ok.all():
+    if not legal.all():
+        ok = np.take(legal, buf) != 0
+        if not ok.all():
+            bad = int(buf[~ok][0])
+            names = ", ".join(ACTION_NAMES[a] for a in bs.spec.action_set)
+            raise ContractError(f"action {ACTION_NAMES[Action(bad)]!r} is not in "
+                                f"{bs.spec.id!r}'s action set ({names})")
+    return bs._stage.upload()
+
+
+def _check_host_actions(bs: BatchState, actions) -> np.ndarray:
+    """The reference's host-side action contract (batch.py:92-106), in one
+    counting pass over the actions."""
+    acts = np.ascontiguousarray(actions, dtype=np.int64)
+    if acts.shape != (bs.n,):
+        raise ContractError(f"actions must have shape ({bs.n},), got {acts.shape}")
+    try:
+        counts = np.bincount(acts, minlength=L.A_COUNT)
+    except ValueError:  # a negative tag
+        raise ContractError(f"action tags must be in [0, {L.A_COUNT})") from None
+    if counts.shape[0] > L.A_COUNT:
+        raise ContractError(f"action tags must be in [0, {L.A_COUNT})")
+    legal = bs.spec.tables.legal
+    if (counts[legal == 0] != 0).any():
+        ok = np.take(legal, acts) != 0
         bad = int(acts[~ok][0])
         names = ", ".join(ACTION_NAMES[a] for a in bs.spec.action_set)
         raise ContractError(f"action {ACTION_NAMES[Action(bad)]!r} is not in "
                             f"{bs.spec.id!r}'s action set ({names})")
+    return acts
+
+
+def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
+                    reuse: bool = False) -> tuple[BatchState, np.ndarray, np.ndarray]:
+    """batch_step with the reference's return types: host actions in, numpy
+    ``(rewards f64[N], dones bool[N])`` out (batch.py:136-138), the state and
+    frames staying on the GPU. One native call does H2D + fused step + D2H +
+    sync (tc_batch_step_host)."""
+    spec, t = bs.spec, bs.spec.tables
+    acts = _check_host_actions(bs, actions)
+    if reuse and bs._retired:
+        sb, ob = bs._retired
+    else:
+        sb = DeviceState.alloc(bs.n, t.n_doors, t.n_entities, bs.device)
+        ob = DeviceOut.alloc(bs.n, t.obs_height, t.obs_width, bs.device,
+                             debug=bs._ob.zbuf is not None)
     if bs._stage is None:
         bs._stage = _ActionStage(bs.n, bs.device)
-    return bs._stage.put(acts)
+    stg = bs._stage
+    np.copyto(stg.h_act, acts)  # pinned staging: async DMA both ways
+    # the ctypes argument tuple of a (state in, state out) pair is built once
+    key = (id(bs._sb), id(sb), id(ob), validate)
+    args = stg.calls.get(key)
+    if args is None:
+        args = (bs._ds.handle, N.C.byref(bs._sb.c_struct()), N.C.byref(sb.c_struct()),
+                stg.h_act_ptr, stg.dev_ptr, N.C.byref(ob.c_struct()), bs.n, 1,
+                1 if validate else 0, N.ptr(bs._counters), stg.h_rew_ptr, stg.h_done_ptr,
+                stream_ptr(bs.device))
+        if len(stg.calls) > 8:
+            stg.calls.clear()
+        stg.calls[key] = (args, bs._sb, sb, ob)  # keep the blocks alive with the key
+    else:
+        args = args[0]
+    if torch.cuda.current_device() == bs.device.index:
+        rc = N.lib().tc_batch_step_host(*args)
+    else:
+        with torch.cuda.device(bs.device):
+            rc = N.lib().tc_batch_step_host(*args)
+    N.check(rc, "tc_batch_step_host")
+    rewards = stg.h_rew.copy()
+    dones = stg.h_done.copy()
+    new = BatchState(spec=spec, n=bs.n, _ds=bs._ds, _sb=sb, _ob=ob, _counters=bs._counters,
+                     base=bs.base, n_total=bs.n_total,
+                     _retired=(bs._sb, bs._ob) if reuse else (), _stage=bs._stage)
+    if validate:
+        new.check()
+    return new, rewards, dones
 
 
 def batch_step(bs: BatchState, actions: Sequence[Action | int] | np.ndarray | torch.Tensor, *,

@@ -1919,6 +1919,36 @@ int tc_batch_step_into(const tc_spec* s, const tc_state* state_in, const tc_stat
                              auto_reset, validate, counters_dev, stream);
 }
 
+int tc_batch_step_host(const tc_spec* s, const tc_state* state_in, const tc_state* state_out,
+                       const int64_t* actions_host, int64_t* actions_dev, const tc_out* out,
+                       int64_t n, int32_t auto_reset, int32_t validate,
+                       tc_counters* counters_dev, double* rewards_host, uint8_t* dones_host,
+                       void* stream) {
+  if (!actions_host || !actions_dev) return fail(TC_E_INVALID, "NULL actions buffer");
+  if (n <= 0) return n == 0 ? TC_OK : fail(TC_E_INVALID, "n must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  TC_CUDA(cudaMemcpyAsync(actions_dev, actions_host, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+  const int rc = launch_batch_kernel(s, state_in, state_out ? state_out : state_in, actions_dev,
+                                     out, n, TC_MODE_STEP, auto_reset, validate, counters_dev,
+                                     stream);
+  if (rc != TC_OK) return rc;
+  // one copy when the host and device result buffers are both laid out as
+  // [rewards f64[n] | dones u8[n]] (the Python host layer allocates them so)
+  if (rewards_host && dones_host &&
+      reinterpret_cast<uint8_t*>(out->rewards) + (size_t)n * 8 == out->dones &&
+      reinterpret_cast<uint8_t*>(rewards_host) + (size_t)n * 8 == dones_host) {
+    TC_CUDA(cudaMemcpyAsync(rewards_host, out->rewards, (size_t)n * 9, cudaMemcpyDeviceToHost, st));
+  } else {
+    if (rewards_host)
+      TC_CUDA(cudaMemcpyAsync(rewards_host, out->rewards, (size_t)n * 8, cudaMemcpyDeviceToHost,
+                              st));
+    if (dones_host)
+      TC_CUDA(cudaMemcpyAsync(dones_host, out->dones, (size_t)n, cudaMemcpyDeviceToHost, st));
+  }
+  TC_CUDA(cudaStreamSynchronize(st));
+  return TC_OK;
+}
+
 int tc_rollout(const tc_spec* s, const tc_state* state, const tc_out* out, int64_t n,
                int64_t base, int64_t n_total, uint64_t policy_key, int64_t step0,
                int32_t k_steps, int32_t frame_ring, tc_counters* counters_dev, void* stream) {

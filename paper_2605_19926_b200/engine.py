@@ -145,10 +145,13 @@ class DeviceOut:
 
     @staticmethod
     def alloc(n: int, obs_h: int, obs_w: int, device, debug: bool = False) -> DeviceOut:
+        # rewards (f64) and dones (u8) share one allocation so a host read of
+        # a step's results is a single D2H copy
+        res = torch.zeros(n * 9, dtype=torch.uint8, device=device)
         o = DeviceOut(
             frames=torch.empty((n, obs_h, obs_w, 3), dtype=torch.uint8, device=device),
-            rewards=torch.zeros(n, dtype=torch.float64, device=device),
-            dones=torch.zeros(n, dtype=torch.uint8, device=device),
+            rewards=res[:8 * n].view(torch.float64),
+            dones=res[8 * n:],
             truncs=torch.zeros(n, dtype=torch.uint8, device=device),
             events=torch.zeros(n, dtype=torch.int32, device=device),
             statuses=torch.zeros(n, dtype=torch.int32, device=device))

@@ -260,3 +260,22 @@ def test_large_batch_matches_oracle_sample():
     """BASELINE C2 size (4096 envs): full bit-exact compare on every 10th step."""
     spec = tc.make_env("my-way-home")
     _compare_rollout(spec, 4096, 30, seed=0, check_every=10)
+
+
+def test_batch_step_host_matches_device_path():
+    spec = tc.make_env("key-door", max_steps=25)
+    n, steps = 300, 40
+    acts = tc.policy_actions(spec, n, steps, 2)
+    a = tc.batch_reset(spec, n, 2, device=DEV)
+    b = tc.batch_reset(spec, n, 2, device=DEV)
+    for s in range(steps):
+        a, ra, da = tc.batch_step(a, acts[s], reuse=True)
+        b, rb, db = tc.batch_step_host(b, acts[s], reuse=True)
+        assert isinstance(rb, np.ndarray) and rb.dtype == np.float64 and db.dtype == np.bool_
+        assert np.array_equal(ra.cpu().numpy(), rb) and np.array_equal(da.cpu().numpy(), db)
+        assert torch.equal(a.frames, b.frames)
+    ha, hb = a.host_state(), b.host_state()
+    for k in ha:
+        assert np.array_equal(ha[k], hb[k]), k
+    with pytest.raises(tc.ContractError):
+        tc.batch_step_host(b, [int(tc.Action.STRAFE_LEFT)] * n)
