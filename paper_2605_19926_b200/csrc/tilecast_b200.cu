@@ -653,6 +653,60 @@ __device__ __forceinline__ March march(const uint32_t* __restrict__ solid, int m
   return r;
 }
 
+// Two rays marched in lockstep (sealed-map fast path): the two dependency
+// chains interleave, hiding latency when few warps share the SM. Each ray
+// follows exactly the same sequence of operations as march<false>.
+struct RaySetup {
+  double sdx, sdy, ddx, ddy;
+  int stepx, dyi, idx;
+};
+__device__ __forceinline__ RaySetup ray_setup(int mw, double ox, double oy, int mapx0, int mapy0,
+                                              double rx, double ry) {
+  RaySetup r;
+  int stepy;
+  if (rx != 0.0) {
+    r.ddx = fabs(1.0 / rx);
+    r.stepx = rx > 0.0 ? 1 : -1;
+    r.sdx = rx > 0.0 ? (((double)mapx0 + 1.0) - ox) * r.ddx : (ox - (double)mapx0) * r.ddx;
+  } else {
+    r.ddx = dinf(); r.stepx = 0; r.sdx = dinf();
+  }
+  if (ry != 0.0) {
+    r.ddy = fabs(1.0 / ry);
+    stepy = ry > 0.0 ? 1 : -1;
+    r.sdy = ry > 0.0 ? (((double)mapy0 + 1.0) - oy) * r.ddy : (oy - (double)mapy0) * r.ddy;
+  } else {
+    r.ddy = dinf(); stepy = 0; r.sdy = dinf();
+  }
+  r.dyi = stepy * mw;
+  r.idx = mapy0 * mw + mapx0;
+  return r;
+}
+
+__device__ __forceinline__ void march2(const uint32_t* __restrict__ solid, uint32_t dmask,
+                                       RaySetup& a, RaySetup& b, March& ra, March& rb) {
+  bool la = true, lb = true, xa = false, xb = false;
+  int sa = 0, sb = 0;
+  do {
+    if (la) {
+      xa = a.sdx < a.sdy;
+      if (xa) { a.sdx += a.ddx; a.idx += a.stepx; } else { a.sdy += a.ddy; a.idx += a.dyi; }
+      sa += 1;
+    }
+    if (lb) {
+      xb = b.sdx < b.sdy;
+      if (xb) { b.sdx += b.ddx; b.idx += b.stepx; } else { b.sdy += b.ddy; b.idx += b.dyi; }
+      sb += 1;
+    }
+    if (la) la = !stops(solid[a.idx], dmask);
+    if (lb) lb = !stops(solid[b.idx], dmask);
+  } while (la || lb);
+  ra.sdx = a.sdx; ra.sdy = a.sdy; ra.ddx = a.ddx; ra.ddy = a.ddy;
+  ra.idx = a.idx; ra.steps = sa; ra.status = TC_ST_OK; ra.xs = xa;
+  rb.sdx = b.sdx; rb.sdy = b.sdy; rb.ddx = b.ddx; rb.ddy = b.ddy;
+  rb.idx = b.idx; rb.steps = sb; rb.status = TC_ST_OK; rb.xs = xb;
+}
+
 // Wall pass: lane L casts the rays of columns L + 32j; per-column spans,
 // colours and zbuf go to shared memory (_pycore.py:153-190). Returns the
 // status of the first failing column (warp-uniform).
@@ -668,12 +722,8 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
   const int ox = (int)floor(e.x), oy = (int)floor(e.y);
   const double atten = S.fc[FC_ATTEN];
   int bad_col = 0x7fffffff, bad_status = TC_ST_OK;
-#pragma unroll 1
-  for (int c = lane; c < W; c += G) {
-    const double k = S.coef[c];
-    const double rx = e.dx + planex * k;
-    const double ry = e.dy + planey * k;
-    const March r = march<CHECKED>(solid, mw, S.h, e.dmask, e.x, e.y, ox, oy, rx, ry);
+  // per-column result -> zbuf / spans / shaded colour, _pycore.py:159-178
+  auto column_out = [&](int c, const March& r) {
     if (rayinfo) {
       int mx, my;
       if (CHECKED && r.status != TC_ST_OK) { mx = (int)r.sdx; my = (int)r.sdy; }
@@ -683,12 +733,11 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     }
     if (CHECKED && r.status != TC_ST_OK) {
       if (c < bad_col) { bad_col = c; bad_status = r.status; }
-      continue;
+      return;
     }
     const double perp = r.xs ? r.sdx - r.ddx : r.sdy - r.ddy;
     sm.zbuf(S)[c] = perp;
     if (zbuf_out) zbuf_out[c] = perp;
-    // _pycore.py:162-178
     const double shade = 1.0 / (1.0 + atten * perp);
     const uint32_t cw = cell[r.idx];
     const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
@@ -701,6 +750,28 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     sm.t0(S)[c] = (uint16_t)(top > 0 ? top : 0);
     sm.t8(S)[c] = (uint8_t)(top > 0 ? top : 0);
     sm.b0(S)[c] = (uint16_t)(bot < H ? bot : H);
+  };
+  int c = lane;
+  if (!CHECKED) {
+    // pairs of columns (c, c + G) marched in lockstep
+#pragma unroll 1
+    for (; c + G < W; c += 2 * G) {
+      const double k0 = S.coef[c], k1 = S.coef[c + G];
+      RaySetup a = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k0, e.dy + planey * k0);
+      RaySetup b = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k1, e.dy + planey * k1);
+      March ra, rb;
+      march2(solid, e.dmask, a, b, ra, rb);
+      column_out(c, ra);
+      column_out(c + G, rb);
+    }
+  }
+#pragma unroll 1
+  for (; c < W; c += G) {
+    const double k = S.coef[c];
+    const double rx = e.dx + planex * k;
+    const double ry = e.dy + planey * k;
+    const March r = march<CHECKED>(solid, mw, S.h, e.dmask, e.x, e.y, ox, oy, rx, ry);
+    column_out(c, r);
   }
   // pad columns so 4-wide loads past W read harmless data
   if (lane < ((W + 3) & ~3) - W) {
@@ -1340,7 +1411,7 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
 // A group of G lanes owns one env at a time (G = 32: a warp; G = 16: each
 // half of a warp runs its own env).
 template <int NC, int G>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, G == 16 ? 4 : TC_MIN_CTAS)
 batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
              const __grid_constant__ StateDev so, const long long* __restrict__ actions,
              const __grid_constant__ OutDev out,
@@ -1444,7 +1515,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
 // K fused steps with on-device policy actions (batch.py:141-153 draws) and
 // auto-reset; the env's state stays in registers across steps.
 template <int NC, int G>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS)
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, G == 16 ? 4 : TC_MIN_CTAS)
 rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
                const __grid_constant__ OutDev out, long long n,
                const __grid_constant__ RolloutArgs ra, tc_counters* __restrict__ counters) {
