@@ -279,3 +279,38 @@ def test_batch_step_host_matches_device_path():
         assert np.array_equal(ha[k], hb[k]), k
     with pytest.raises(tc.ContractError):
         tc.batch_step_host(b, [int(tc.Action.STRAFE_LEFT)] * n)
+
+
+def test_gym_vecenv_and_env_match_core():
+    from paper_2605_19926_b200 import gym
+    spec = tc.make_env("simple", max_steps=30)
+    n, steps = 8, 50
+    tags = np.array([int(a) for a in spec.action_set])
+    rnd = np.random.default_rng(0)
+    idx = rnd.integers(0, len(tags), size=(steps, n))
+    v = gym.make_vec("simple", n, seed=3, max_steps=30)
+    vd = gym.make_vec("simple", n, seed=3, max_steps=30)
+    bs = tc.batch_reset(spec, n, 3, device=DEV)
+    for s in range(steps):
+        obs, r, d, info = v.step(idx[s])
+        obs2, r2, d2, _ = vd.step(torch.as_tensor(idx[s], device=DEV))
+        bs, rr, dd = tc.batch_step(bs, tags[idx[s]])
+        assert torch.equal(obs, bs.frames) and torch.equal(obs2, bs.frames)
+        assert torch.equal(r, rr) and torch.equal(d, dd) and torch.equal(r2, rr)
+    v.check()
+    vd.check()
+    e = gym.make("simple", max_steps=30)
+    obs, _ = e.reset(seed=3)
+    assert np.array_equal(obs, tc.batch_reset(spec, 1, 3, device=DEV).frames[0].cpu().numpy())
+    o, rwd, term, trunc, info = e.step(0)
+    assert o.shape == (64, 64, 3) and isinstance(rwd, float)
+
+
+def test_cli_bench_report_schema():
+    from paper_2605_19926_b200 import cli
+    rep = cli.bench("key-door", 64, 20, 0, 64, 64)
+    assert rep["schema_version"] == 1 and rep["kind"] == "bench"
+    assert set(rep["config"]) >= {"env", "n", "steps", "seed", "width", "height", "threads"}
+    assert set(rep["results"]) >= {"steps_per_second", "frames_per_second", "us_per_frame",
+                                   "reward_sum"}
+    assert rep["results"]["steps_per_second"] > 0
