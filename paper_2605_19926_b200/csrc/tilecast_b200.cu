@@ -1176,7 +1176,8 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
       uint8_t* top = frame + (size_t)rowoff * row_bytes + cg * 48;
       uint8_t* bot = frame + (size_t)(H - 1 - rowoff) * row_bytes + cg * 48;
       const size_t step = (size_t)RPI * row_bytes;
-      for (int r = rowoff; r < h2; r += RPI, top += step, bot -= step) {
+      // one row pair (row r and its mirror H-1-r) -> 6 x 16-byte stores
+      auto row_out = [&](int r, uint8_t* top_p, uint8_t* bot_p) {
         const uint32_t R = 0x80808080u + (uint32_t)r * 0x01010101u;
         uint32_t tw[12], bw[12];
 #pragma unroll
@@ -1191,15 +1192,23 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
           bw[3 * j + 1] = (m1 & Wd[3 * j + 1]) | (~m1 & fw1);
           bw[3 * j + 2] = (m2 & Wd[3 * j + 2]) | (~m2 & fw2);
         }
-        uint4* dt = reinterpret_cast<uint4*>(top);
-        uint4* db = reinterpret_cast<uint4*>(bot);
+        uint4* dt = reinterpret_cast<uint4*>(top_p);
+        uint4* db = reinterpret_cast<uint4*>(bot_p);
         TC_STORE(dt + 0, make_uint4(tw[0], tw[1], tw[2], tw[3]));
         TC_STORE(dt + 1, make_uint4(tw[4], tw[5], tw[6], tw[7]));
         TC_STORE(dt + 2, make_uint4(tw[8], tw[9], tw[10], tw[11]));
         TC_STORE(db + 0, make_uint4(bw[0], bw[1], bw[2], bw[3]));
         TC_STORE(db + 1, make_uint4(bw[4], bw[5], bw[6], bw[7]));
         TC_STORE(db + 2, make_uint4(bw[8], bw[9], bw[10], bw[11]));
+      };
+      // two row pairs per trip (independent registers) so a trip's compute
+      // does not wait for the previous trip's stores to release theirs
+      int r = rowoff;
+      for (; r + RPI < h2; r += 2 * RPI, top += 2 * step, bot -= 2 * step) {
+        row_out(r, top, bot);
+        row_out(r + RPI, top + step, bot - step);
       }
+      if (r < h2) row_out(r, top, bot);
     }
   }
   if (m > 0) {
