@@ -279,27 +279,6 @@ __device__ __forceinline__ RayHit cast_ray(const uint32_t* __restrict__ cell, in
   return r;
 }
 
-// _pycore.py:99-129, split so per-column (aa, ea) and per-row (v, ev) terms
-// are computed once and reused: identical doubles, identical comparisons.
-__device__ __forceinline__ int sprite_mask(int kd, double aa, double ea, double v, double ev) {
-  if (kd == K_GOAL) {
-    double dv = v - 0.5;
-    if (dv < 0.0) dv = -dv;
-    return (aa + dv * 2.0 <= 0.8) ? 1 : 0;
-  }
-  if (kd == K_KEY) {
-    const double e = ea * ea + ev * ev;
-    if (0.30 <= e && e <= 1.0) return 1;
-    if (aa <= 0.07 && 0.30 <= v && v <= 0.85) return 1;
-    if (aa <= 0.24 && 0.62 <= v && v <= 0.70) return 1;
-    if (aa <= 0.24 && 0.76 <= v && v <= 0.84) return 1;
-    return 0;
-  }
-  if (aa <= 0.10 && 0.32 <= v && v <= 0.73) return 1;
-  if (aa <= 0.38 && 0.47 <= v && v <= 0.60) return 1;
-  if (aa <= 0.60 && 0.25 <= v && v <= 0.80) return 2;
-  return 0;
-}
 
 // One pass over the <= 2x2 tiles the disc (cx, cy, radius) overlaps, doing
 // _touch_doors (_pycore.py:307-343; only when `touch`) and then _blocked
@@ -931,42 +910,77 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
       if (band == nullptr) continue;
       const int ra = max(r.r0, r_lo), rb = min(r.r1, r_lo + rows);
       if (ra >= rb) continue;
-      double aa[NC], ea[NC];
+      // per-column terms: goal -> aa; key -> (aa/0.30)^2 and rectangle
+      // flags aa<=0.07 | aa<=0.24 | aa<=0.24; medkit -> aa<=0.10 | aa<=0.38 |
+      // aa<=0.60 (_pycore.py:99-129 split into column and row factors)
+      double ct[NC];
+      int cf[NC];
       bool vis[NC];
       bool anyv = false;
 #pragma unroll
       for (int j = 0; j < NC; j++) {
         const int c = lane + G * j;
         vis[j] = false;
-        aa[j] = 0.0;
-        ea[j] = 0.0;
+        ct[j] = 0.0;
+        cf[j] = 0;
         if (c < W && !(sm.zbuf(S)[c] <= r.dep)) {
           const double a = (S.coef[c] - r.ks) / r.halfk;
           if (!(a <= -1.0 || a >= 1.0)) {
             vis[j] = true;
-            aa[j] = a >= 0.0 ? a : -a;
-            if (key) ea[j] = aa[j] / 0.30;
+            const double aa = a >= 0.0 ? a : -a;
+            if (r.kd == K_GOAL) {
+              ct[j] = aa;
+            } else if (key) {
+              const double ea = aa / 0.30;
+              ct[j] = ea * ea;
+              cf[j] = (aa <= 0.07 ? 1 : 0) | (aa <= 0.24 ? 6 : 0);
+            } else {
+              cf[j] = (aa <= 0.10 ? 1 : 0) | (aa <= 0.38 ? 2 : 0) | (aa <= 0.60 ? 4 : 0);
+            }
           }
         }
         anyv |= vis[j];
       }
       if (!g.any(anyv)) continue;
       for (int r32 = ra; r32 < rb; r32 += G) {
-        // lane-parallel row terms for rows r32 .. r32+G-1
-        double v_l = 0.0, ev_l = 0.0;
+        // lane-parallel row terms for rows r32 .. r32+G-1: goal -> |v-0.5|*2;
+        // key -> ((v-0.30)/0.18)^2 and v-range flags; medkit -> v-range flags
+        double rt_l = 0.0;
+        int rf_l = 0;
         if (r32 + lane < rb) {
-          v_l = ((double)(r32 + lane - r.vtop) + 0.5) / denom;
-          if (key) ev_l = (v_l - 0.30) / 0.18;
+          const double v = ((double)(r32 + lane - r.vtop) + 0.5) / denom;
+          if (r.kd == K_GOAL) {
+            double dv = v - 0.5;
+            if (dv < 0.0) dv = -dv;
+            rt_l = dv * 2.0;
+          } else if (key) {
+            const double ev = (v - 0.30) / 0.18;
+            rt_l = ev * ev;
+            rf_l = (0.30 <= v && v <= 0.85 ? 1 : 0) | (0.62 <= v && v <= 0.70 ? 2 : 0) |
+                   (0.76 <= v && v <= 0.84 ? 4 : 0);
+          } else {
+            rf_l = (0.32 <= v && v <= 0.73 ? 1 : 0) | (0.47 <= v && v <= 0.60 ? 2 : 0) |
+                   (0.25 <= v && v <= 0.80 ? 4 : 0);
+          }
         }
         const int nr = min(G, rb - r32);
         for (int k = 0; k < nr; k++) {
-          const double v = g.shfl(v_l, k);
-          const double ev = g.shfl(ev_l, k);
+          const double rt = g.shfl(rt_l, k);
+          const int rf = g.shfl(rf_l, k);
           uint8_t* drow = band + (r32 + k - r_lo) * row_bytes;
 #pragma unroll
           for (int j = 0; j < NC; j++) {
             if (!vis[j]) continue;
-            const int mk = sprite_mask(r.kd, aa[j], ea[j], v, ev);
+            int mk;
+            if (r.kd == K_GOAL) {
+              mk = (ct[j] + rt <= 0.8) ? 1 : 0;  // aa + |v-0.5|*2.0 <= 0.8
+            } else if (key) {
+              const double e = ct[j] + rt;        // ea*ea + ev*ev
+              mk = ((0.30 <= e && e <= 1.0) || (cf[j] & rf) != 0) ? 1 : 0;
+            } else {
+              const int x = cf[j] & rf;
+              mk = (x & 3) ? 1 : ((x & 4) ? 2 : 0);
+            }
             if (mk) {
               const uint32_t col = mk == 1 ? r.s1 : r.s2;
               uint8_t* d = drow + (lane + G * j) * 3;
@@ -1225,7 +1239,7 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
                                                  int& buf, const LaneGeo& lg) {
   const Grp<G> g;
   const int lane = g.lane;
-  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
+  const int W = S.obs_w, H = S.obs_h;
   if (S.mirror) {
     if (S.direct == 1) mirror_direct<NC, G>(S, sm, m, frame, lg);
     else mirror_bands<NC, true, G>(S, sm, m, frame, bulk_pending, buf, lg);
