@@ -60,6 +60,9 @@ constexpr int WARPS_PER_CTA = 4;
 #ifndef TC_TRACE
 #define TC_TRACE 0  // perf experiments only: per-env phase timestamps
 #endif
+#ifndef TC_LOCKSTEP
+#define TC_LOCKSTEP 2  // rays per lane marched in lockstep on sealed maps
+#endif
 #ifndef TC_STORE
 #define TC_STORE __stcs  // frame stores (direct path): streaming / evict-first
 #endif
@@ -686,6 +689,38 @@ __device__ __forceinline__ void march2(const uint32_t* __restrict__ solid, uint3
   rb.idx = b.idx; rb.steps = sb; rb.status = TC_ST_OK; rb.xs = xb;
 }
 
+template <int R>
+__device__ __forceinline__ void march_n(const uint32_t* __restrict__ solid, uint32_t dmask,
+                                        RaySetup (&a)[R], March (&out)[R]) {
+  bool live[R], xs[R];
+  int st[R];
+#pragma unroll
+  for (int q = 0; q < R; q++) { live[q] = true; xs[q] = false; st[q] = 0; }
+  bool any;
+  do {
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      if (live[q]) {
+        xs[q] = a[q].sdx < a[q].sdy;
+        if (xs[q]) { a[q].sdx += a[q].ddx; a[q].idx += a[q].stepx; }
+        else { a[q].sdy += a[q].ddy; a[q].idx += a[q].dyi; }
+        st[q] += 1;
+      }
+    }
+    any = false;
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      if (live[q]) live[q] = !stops(solid[a[q].idx], dmask);
+      any |= live[q];
+    }
+  } while (any);
+#pragma unroll
+  for (int q = 0; q < R; q++) {
+    out[q].sdx = a[q].sdx; out[q].sdy = a[q].sdy; out[q].ddx = a[q].ddx; out[q].ddy = a[q].ddy;
+    out[q].idx = a[q].idx; out[q].steps = st[q]; out[q].status = TC_ST_OK; out[q].xs = xs[q];
+  }
+}
+
 // Wall pass: lane L casts the rays of columns L + 32j; per-column spans,
 // colours and zbuf go to shared memory (_pycore.py:153-190). Returns the
 // status of the first failing column (warp-uniform).
@@ -732,7 +767,21 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
   };
   int c = lane;
   if (!CHECKED) {
-    // pairs of columns (c, c + G) marched in lockstep
+    // groups of TC_LOCKSTEP columns (c, c + G, ...) marched in lockstep
+    constexpr int LR = TC_LOCKSTEP;
+#pragma unroll 1
+    for (; c + (LR - 1) * G < W; c += LR * G) {
+      RaySetup rs[LR];
+      March rr[LR];
+#pragma unroll
+      for (int q = 0; q < LR; q++) {
+        const double k = S.coef[c + q * G];
+        rs[q] = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k, e.dy + planey * k);
+      }
+      march_n<LR>(solid, e.dmask, rs, rr);
+#pragma unroll
+      for (int q = 0; q < LR; q++) column_out(c + q * G, rr[q]);
+    }
 #pragma unroll 1
     for (; c + G < W; c += 2 * G) {
       const double k0 = S.coef[c], k1 = S.coef[c + G];
