@@ -1497,7 +1497,12 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
   const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
   const uint32_t *cell, *solid;
+  // programmatic dependent launch: let the next step's grid start its
+  // prologue as our CTAs retire, and stage the (constant) map before
+  // waiting for the previous step's state to be complete and visible
+  asm volatile("griddepcontrol.launch_dependents;");
   stage_map(S, smap, cell, solid);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
   const LaneGeo lg = lane_geo<G>(S);
@@ -1683,6 +1688,11 @@ struct tc_spec {
 namespace {
 
 thread_local std::string g_err;
+// programmatic dependent launch of consecutive steps (TILECAST_PDL=0 disables)
+const bool g_pdl = [] {
+  const char* e = getenv("TILECAST_PDL");
+  return e ? atoi(e) != 0 : true;
+}();
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -2041,8 +2051,17 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
   int m = mode, ar = auto_reset, va = validate;
   SpecDev spec = d;
   void* args[] = {&spec, &sd, &so, &acts, &od, (void*)&nn, &m, &ar, &va, &counters_dev};
-  TC_CUDA(cudaLaunchKernel(select_batch(s->nc, s->dev.group), dim3(grid),
-                           dim3(WARPS_PER_CTA * 32), args, s->smem_bytes, (cudaStream_t)stream));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(WARPS_PER_CTA * 32);
+  cfg.dynamicSmemBytes = s->smem_bytes;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TC_CUDA(cudaLaunchKernelExC(&cfg, select_batch(s->nc, s->dev.group), args));
   return TC_OK;
 }
 
