@@ -504,6 +504,11 @@ struct WarpSmem {
 
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 
+// wall colours are stored 16 columns per 20-word block (4 words of pad) so
+// the per-16-column uint4 loads of neighbouring column groups fall in
+// different bank quads (stride 20 words: 5*cg mod 8 is a permutation)
+__host__ __device__ __forceinline__ int wslot(int c) { return c + ((c >> 4) << 2); }
+
 // per-warp shared-memory layout; returns the window size. nbands = staging
 // buffers (0 for the direct-store compose).
 __host__ inline int warp_smem_layout(SpecDev& d, int nbands) {
@@ -513,7 +518,7 @@ __host__ inline int warp_smem_layout(SpecDev& d, int nbands) {
   d.o_t0 = off; off += align16(wp * 2);
   d.o_b0 = off; off += align16(wp * 2);
   d.o_t8 = off; off += align16(wp);
-  d.o_wrgb = off; off += align16(wp * 4);
+  d.o_wrgb = off; off += align16((wp / 16) * 20 * 4 + 64);
   d.o_zbuf = off; off += align16(wp * 8);
   d.o_gdep = off; off += align16(e * 8);
   d.o_recs = off; off += align16(e * (int)sizeof(SpriteRec));
@@ -756,7 +761,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     const uint32_t cw = cell[r.idx];
     const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
                                                                      : S.pal[cw & 0xffu];
-    sm.wrgb(S)[c] = rgb_scale(base, shade);
+    sm.wrgb(S)[wslot(c)] = rgb_scale(base, shade);
     double lh_f = (double)H / perp;
     if (lh_f > 1e9) lh_f = 1e9;
     const int half = (int)lh_f / 2;
@@ -803,7 +808,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
   }
   // pad columns so 4-wide loads past W read harmless data
   if (lane < ((W + 3) & ~3) - W) {
-    sm.t0(S)[W + lane] = (uint16_t)h2; sm.b0(S)[W + lane] = (uint16_t)h2; sm.wrgb(S)[W + lane] = 0;
+    sm.t0(S)[W + lane] = (uint16_t)h2; sm.b0(S)[W + lane] = (uint16_t)h2; sm.wrgb(S)[wslot(W + lane)] = 0;
   }
   if (!CHECKED) return TC_ST_OK;
   const int first_bad = g.min(bad_col);
@@ -1136,7 +1141,7 @@ __device__ __forceinline__ void mirror_bands(const SpecDev& S, const WarpSmem& s
       if (rowoff < RPI) {
         for (int cg = cg0; cg < CG; cg += G) {
           const uint4 T = *reinterpret_cast<const uint4*>(sm.t8(S) + 16 * cg);
-          const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 16 * cg);
+          const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 20 * cg);
           uint32_t Wd[12];
 #pragma unroll
           for (int j = 0; j < 4; j++) {
@@ -1226,7 +1231,7 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
   if (rowoff < RPI) {
     for (int cg = lg.cg0; cg < CG; cg += G) {
       const uint4 T = *reinterpret_cast<const uint4*>(sm.t8(S) + 16 * cg);
-      const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 16 * cg);
+      const uint4* wp = reinterpret_cast<const uint4*>(sm.wrgb(S) + 20 * cg);
       uint32_t Wd[12];
 #pragma unroll
       for (int j = 0; j < 4; j++) {
@@ -1330,7 +1335,7 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
         for (int q = q_first; q < Q; q += G) {
           const uint2 t4 = *reinterpret_cast<const uint2*>(sm.t0(S) + 4 * q);
           const uint2 b4 = *reinterpret_cast<const uint2*>(sm.b0(S) + 4 * q);
-          const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb(S) + 4 * q);
+          const uint4 w4 = *reinterpret_cast<const uint4*>(sm.wrgb(S) + wslot(4 * q));
           const int t0 = t4.x & 0xffff, t1 = t4.x >> 16, t2 = t4.y & 0xffff, t3 = t4.y >> 16;
           const int b0 = b4.x & 0xffff, b1 = b4.x >> 16, b2 = b4.y & 0xffff, b3 = b4.y >> 16;
           const uint32_t w0w = __byte_perm(w4.x, w4.y, 0x4210),
@@ -1361,7 +1366,7 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
       for (int p = lane; p < items; p += G) {
         const int rr = p / W, c = p - rr * W;
         const uint32_t row = (uint32_t)(r_lo + rr);
-        const uint32_t col = row < sm.t0(S)[c] ? C : (row < sm.b0(S)[c] ? sm.wrgb(S)[c] : F);
+        const uint32_t col = row < sm.t0(S)[c] ? C : (row < sm.b0(S)[c] ? sm.wrgb(S)[wslot(c)] : F);
         uint8_t* d = band + rr * row_bytes + c * 3;
         d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
       }
