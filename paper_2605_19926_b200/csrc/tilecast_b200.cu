@@ -29,6 +29,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -694,6 +695,11 @@ __device__ __forceinline__ void march2(const uint32_t* __restrict__ solid, uint3
   rb.idx = b.idx; rb.steps = sb; rb.status = TC_ST_OK; rb.xs = xb;
 }
 
+// R rays marched in lockstep: independent fp64 chains interleave. Each ray
+// performs exactly the reference's additions in the reference's order. (A
+// software-pipelined variant that issues step k+1's stop-code load before
+// step k's test -- the stop-code array keeps the w+1-cell wall guards it
+// needs -- measured no faster on B200.)
 template <int R>
 __device__ __forceinline__ void march_n(const uint32_t* __restrict__ solid, uint32_t dmask,
                                         RaySetup (&a)[R], March (&out)[R]) {
@@ -706,7 +712,7 @@ __device__ __forceinline__ void march_n(const uint32_t* __restrict__ solid, uint
 #pragma unroll
     for (int q = 0; q < R; q++) {
       if (live[q]) {
-        xs[q] = a[q].sdx < a[q].sdy;
+        xs[q] = a[q].sdx < a[q].sdy;  // ties step Y (_pycore.py:70)
         if (xs[q]) { a[q].sdx += a[q].ddx; a[q].idx += a[q].stepx; }
         else { a[q].sdy += a[q].ddy; a[q].idx += a[q].dyi; }
         st[q] += 1;
@@ -1472,14 +1478,14 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
     solid = S.solid;
     return;
   }
-  const int cells = S.h * S.w;
-  for (int k = threadIdx.x; k < cells; k += blockDim.x) {
-    smap[k] = S.cell[k];
-    smap[cells + k] = S.solid[k];
-  }
+  const int cells = S.h * S.w, guard = S.w + 1;
+  for (int k = threadIdx.x; k < cells; k += blockDim.x) smap[k] = S.cell[k];
+  // stop codes with their wall guards: [guard | cells | guard]
+  const uint32_t* gsrc = S.solid - guard;
+  for (int k = threadIdx.x; k < cells + 2 * guard; k += blockDim.x) smap[cells + k] = gsrc[k];
   __syncthreads();
   cell = smap;
-  solid = smap + cells;
+  solid = smap + cells + guard;
 }
 
 
@@ -1500,7 +1506,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   const int lane = g.lane;
   const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;  // group id in the CTA
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
-  const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
+  const int map_bytes = S.smem_map ? align16((S.h * S.w * 2 + 2 * (S.w + 1)) * 4) : 0;
   const uint32_t *cell, *solid;
   // programmatic dependent launch: let the next step's grid start its
   // prologue as our CTAs retire, and stage the (constant) map before
@@ -1607,7 +1613,7 @@ rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateD
   const int lane = g.lane;
   const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
-  const int map_bytes = S.smem_map ? align16(S.h * S.w * 8) : 0;
+  const int map_bytes = S.smem_map ? align16((S.h * S.w * 2 + 2 * (S.w + 1)) * 4) : 0;
   const uint32_t *cell, *solid;
   stage_map(S, smap, cell, solid);
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
@@ -1878,7 +1884,7 @@ int launch_geometry(tc_spec* s) {
   if (d.npairs > 4) d.npairs = 4;
   d.warp_smem = warp_smem_layout(d, d.direct == 1 ? 0 : (d.mirror ? 2 * d.npairs : 2));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
-  const size_t map_bytes = d.smem_map ? (size_t)align16(d.h * d.w * 8) : 0;
+  const size_t map_bytes = d.smem_map ? (size_t)align16((d.h * d.w * 2 + 2 * (d.w + 1)) * 4) : 0;
   s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * (32 / d.group) * d.warp_smem;
   s->nc = pick_nc(d.obs_w, d.group);
   const void* fns[2] = {select_batch(s->nc, d.group), select_rollout(s->nc, d.group)};
@@ -1961,7 +1967,10 @@ int tc_spec_create(const tc_tables* t, tc_spec** out) {
 
   BlobBuilder b;
   const size_t o_cell = b.add(cells.data(), cells.size() * 4);
-  const size_t o_solid = b.add(solid.data(), solid.size() * 4);
+  // stop codes with a wall guard of w+1 cells on each side (speculative DDA)
+  std::vector<uint32_t> gsolid(solid.size() + 2 * (size_t)(t->w + 1), 0xffffffffu);
+  std::copy(solid.begin(), solid.end(), gsolid.begin() + (t->w + 1));
+  const size_t o_solid = b.add(gsolid.data(), gsolid.size() * 4) + (size_t)(t->w + 1) * 4;
   const size_t o_pal = b.add(pal.data(), pal.size() * 4);
   const size_t o_door = b.add(doorrgb.data(), doorrgb.size() * 4);
   const size_t o_dcol = b.add(t->dcol, t->n_doors);
