@@ -113,6 +113,7 @@ struct SpecDev {
   int mir_rpi16;     // same for 16-lane groups
   int group;         // lanes per env: 32 (one env per warp) or 16 (two per warp)
   int direct;        // 1 = mirror compose stores straight to HBM (no TMA staging)
+  int contig;        // direct path: lanes store consecutive 16-byte chunks ((W/16) | G)
   int npairs;        // mirror path: staged band pairs in flight (2..4)
   int o_t0, o_b0, o_t8, o_wrgb, o_zbuf, o_gdep, o_recs, o_band;  // WarpSmem offsets
   int warp_smem;     // bytes of per-warp shared memory
@@ -1292,6 +1293,71 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
   g.sync();
 }
 
+// Direct mirrored compose with lane-contiguous stores: the top half of the
+// frame (h2 rows, contiguous in HBM) is cut into 16-byte chunks and lane l
+// of the group writes chunks l, l+G, l+2G, ... so every store instruction
+// covers G x 16 contiguous bytes (2 cache lines for 16 lanes instead of ~8
+// with the per-column layout) and the mirror row's chunk at the same row
+// offset. Needs CPR = 3W/16 chunks per row to divide 3G: then a lane's chunk
+// column repeats with period 3 (phases p) and its rows step by RB = 3G/CPR.
+// A chunk's 4 words span two quads qa, qa+1; one PRMT per word (selectors
+// precomputed per phase) turns the two SWAR row tests into the word's mask.
+template <int NC, int G>
+__device__ __forceinline__ void mirror_contig(const SpecDev& S, const WarpSmem& sm, int m,
+                                              uint8_t* __restrict__ frame) {
+  const Grp<G> g;
+  const int lane = g.lane;
+  const int W = S.obs_w, H = S.obs_h, h2 = H / 2;
+  const int row_bytes = W * 3;
+  const int CPR = row_bytes >> 4;
+  const int RB = 3 * G / CPR;
+  const uint32_t C = S.ceil_rgb, F = S.floor_rgb;
+  const uint32_t* __restrict__ t8w = reinterpret_cast<const uint32_t*>(sm.t8(S));
+  const uint32_t* __restrict__ wc = sm.wrgb(S);
+#pragma unroll 1
+  for (int p = 0; p < 3; p++) {
+    const int c = lane + G * p;
+    const int rp = c / CPR, k = c - rp * CPR;
+    const int qa = (4 * k) / 3;
+    const uint32_t Ta = t8w[qa], Tb = t8w[qa + 1];
+    uint32_t Wd[4], sel[4], cw[4], fw[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int wi = 4 * k + j;      // word index in the row
+      const int q = wi / 3, s = wi - 3 * q;
+      const uint32_t bp = s == 0 ? 0x4210u : (s == 1 ? 0x5421u : 0x6542u);
+      Wd[j] = __byte_perm(wc[wslot(4 * q + s)], wc[wslot(4 * q + s + 1)], bp);
+      cw[j] = __byte_perm(C, C, bp);
+      fw[j] = __byte_perm(F, F, bp);
+      const uint32_t ms = s == 0 ? 0x9888u : (s == 1 ? 0xAA99u : 0xBBBAu);
+      sel[j] = q == qa ? ms : ms + 0x4444u;  // second quad -> bytes 4..7
+    }
+    uint8_t* top = frame + (size_t)rp * row_bytes + 16 * k;
+    uint8_t* bot = frame + (size_t)(H - 1 - rp) * row_bytes + 16 * k;
+    const size_t step = (size_t)RB * row_bytes;
+#pragma unroll 2
+    for (int r = rp; r < h2; r += RB, top += step, bot -= step) {
+      const uint32_t R = 0x80808080u + (uint32_t)r * 0x01010101u;
+      const uint32_t Da = R - Ta, Db = R - Tb;
+      uint32_t tw[4], bw[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        uint32_t mk;
+        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(mk) : "r"(Da), "r"(Db), "r"(sel[j]));
+        tw[j] = (mk & Wd[j]) | (~mk & cw[j]);
+        bw[j] = (mk & Wd[j]) | (~mk & fw[j]);
+      }
+      TC_STORE(reinterpret_cast<uint4*>(top), make_uint4(tw[0], tw[1], tw[2], tw[3]));
+      TC_STORE(reinterpret_cast<uint4*>(bot), make_uint4(bw[0], bw[1], bw[2], bw[3]));
+    }
+  }
+  if (m > 0) {
+    g.sync();
+    draw_sprites<NC, G>(S, sm, m, frame, 0, nullptr, 0, H);
+  }
+  g.sync();
+}
+
 // Phase 3: compose the frame in staged bands, draw sprites, ship with TMA.
 template <int NC, int G>
 __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSmem& sm, int m,
@@ -1301,7 +1367,8 @@ __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSme
   const int lane = g.lane;
   const int W = S.obs_w, H = S.obs_h;
   if (S.mirror) {
-    if (S.direct == 1) mirror_direct<NC, G>(S, sm, m, frame, lg);
+    if (S.direct == 1 && S.contig) mirror_contig<NC, G>(S, sm, m, frame);
+    else if (S.direct == 1) mirror_direct<NC, G>(S, sm, m, frame, lg);
     else mirror_bands<NC, true, G>(S, sm, m, frame, bulk_pending, buf, lg);
     return;
   }
@@ -1512,6 +1579,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   // prologue as our CTAs retire, and stage the (constant) map before
   // waiting for the previous step's state to be complete and visible
   asm volatile("griddepcontrol.launch_dependents;");
+  if ((long long)blockIdx.x >= n) return;  // no env for this CTA (n < grid)
   stage_map(S, smap, cell, solid);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
@@ -1525,7 +1593,10 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   // last CTA to finish zeroes it for the next launch)
   const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
   const bool dyn = counters != nullptr && n > stride;
-  long long i = (long long)blockIdx.x * WARPS_PER_CTA * NG + grp;
+  // first env of each group: interleaved over CTAs (env = grp * grid + cta)
+  // so a partial wave spreads evenly over the SMs instead of filling the
+  // first CTAs
+  long long i = (long long)grp * gridDim.x + blockIdx.x;
   while (i < n) {
     // grab the next ticket now; its latency hides behind this env's work
     long long tnext = i + stride;
@@ -1615,6 +1686,7 @@ rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateD
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
   const int map_bytes = S.smem_map ? align16((S.h * S.w * 2 + 2 * (S.w + 1)) * 4) : 0;
   const uint32_t *cell, *solid;
+  if ((long long)blockIdx.x >= n) return;  // no env for this CTA (n < grid)
   stage_map(S, smap, cell, solid);
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
@@ -1622,7 +1694,7 @@ rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateD
   int bulk_pending = 0, buf = 0;
   uint32_t badbits = 0;
   const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
-  for (long long i = (long long)blockIdx.x * WARPS_PER_CTA * NG + grp; i < n; i += stride) {
+  for (long long i = (long long)grp * gridDim.x + blockIdx.x; i < n; i += stride) {
     Env e;
     int st_acc = TC_ST_OK;
     load_env<G>(S, st, i, e);
@@ -1874,10 +1946,14 @@ int launch_geometry(tc_spec* s) {
   if (d.group != 16 || d.obs_w > 64) d.group = 32;
   // frame store path: 0 = staged bands + TMA bulk stores, 1 = 16-byte stores
   // straight from registers (no staging smem -> more resident envs), 2 =
-  // staged bands + coalesced LDS/STG. Measured best: 1 with 16-lane groups,
-  // 0 with full warps; TILECAST_DIRECT overrides.
+  // staged bands + coalesced LDS/STG, 3 = 1 with the per-column lane layout.
+  // Measured best: 1 whenever the lane-contiguous layout applies ((W/16) | G)
+  // or with 16-lane groups, else 0; TILECAST_DIRECT overrides.
+  const bool contig_ok = d.mirror && d.group % (d.obs_w / 16) == 0;
   const char* dr = getenv("TILECAST_DIRECT");
-  d.direct = d.mirror ? (dr ? atoi(dr) : (d.group == 16 ? 1 : 0)) : 0;
+  d.direct = d.mirror ? (dr ? atoi(dr) : ((d.group == 16 || contig_ok) ? 1 : 0)) : 0;
+  d.contig = d.direct == 1 && contig_ok;
+  if (d.direct == 3) d.direct = 1;
   const char* np = getenv("TILECAST_NPAIRS");
   d.npairs = np ? atoi(np) : 2;
   if (d.npairs < 2) d.npairs = 2;
@@ -1929,7 +2005,12 @@ OutDev to_dev(const tc_out* o) {
 int grid_for(const tc_spec* s, int64_t n) {
   const int per_cta = WARPS_PER_CTA * (32 / s->dev.group);  // envs per CTA pass
   const int64_t want = (n + per_cta - 1) / per_cta;
-  return (int)(want < s->max_ctas ? want : s->max_ctas);
+  if (want >= s->max_ctas) return s->max_ctas;
+  // a partial wave: round the grid up to whole rounds of SMs (envs are
+  // interleaved over CTAs, so every SM gets the same number of envs +-1)
+  const int sms = device_sm_count();
+  const int64_t g = (want + sms - 1) / sms * sms;
+  return (int)(g < s->max_ctas ? g : s->max_ctas);
 }
 
 }  // namespace
