@@ -116,6 +116,7 @@ struct SpecDev {
   int contig;        // direct path: lanes store consecutive 16-byte chunks ((W/16) | G)
   int npairs;        // mirror path: staged band pairs in flight (2..4)
   int o_t0, o_b0, o_t8, o_wrgb, o_zbuf, o_gdep, o_recs, o_band;  // WarpSmem offsets
+  int o_wpk, o_tpk;  // contig compose: packed wall RGB / per-byte top row streams
   int warp_smem;     // bytes of per-warp shared memory
 };
 
@@ -496,6 +497,8 @@ struct WarpSmem {
   __device__ __forceinline__ uint16_t* b0(const SpecDev& S) const { return (uint16_t*)(base + S.o_b0); }
   __device__ __forceinline__ uint8_t* t8(const SpecDev& S) const { return base + S.o_t8; }
   __device__ __forceinline__ uint32_t* wrgb(const SpecDev& S) const { return (uint32_t*)(base + S.o_wrgb); }
+  __device__ __forceinline__ uint8_t* wpk(const SpecDev& S) const { return base + S.o_wpk; }
+  __device__ __forceinline__ uint8_t* tpk(const SpecDev& S) const { return base + S.o_tpk; }
   __device__ __forceinline__ double* zbuf(const SpecDev& S) const { return (double*)(base + S.o_zbuf); }
   __device__ __forceinline__ double* gdep(const SpecDev& S) const { return (double*)(base + S.o_gdep); }
   __device__ __forceinline__ SpriteRec* recs(const SpecDev& S) const { return (SpriteRec*)(base + S.o_recs); }
@@ -525,6 +528,10 @@ __host__ inline int warp_smem_layout(SpecDev& d, int nbands) {
   d.o_gdep = off; off += align16(e * 8);
   d.o_recs = off; off += align16(e * (int)sizeof(SpriteRec));
   d.o_band = off; off += nbands * d.band_stride;
+  // contig compose: the wall colours / tops as byte streams laid out like a
+  // frame row (3 bytes per column)
+  d.o_wpk = off; off += d.contig ? align16(3 * wp) : 0;
+  d.o_tpk = off; off += d.contig ? align16(3 * wp) : 0;
   return align16(off);
 }
 
@@ -768,14 +775,24 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     const uint32_t cw = cell[r.idx];
     const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
                                                                      : S.pal[cw & 0xffu];
-    sm.wrgb(S)[wslot(c)] = rgb_scale(base, shade);
+    const uint32_t rgb = rgb_scale(base, shade);
     double lh_f = (double)H / perp;
     if (lh_f > 1e9) lh_f = 1e9;
     const int half = (int)lh_f / 2;
     const int top = h2 - half, bot = h2 + half;
-    sm.t0(S)[c] = (uint16_t)(top > 0 ? top : 0);
-    sm.t8(S)[c] = (uint8_t)(top > 0 ? top : 0);
-    sm.b0(S)[c] = (uint16_t)(bot < H ? bot : H);
+    if (S.contig) {
+      // mirrored compose reads only the (colour, top) byte streams
+      uint8_t* wp = sm.wpk(S) + 3 * c;
+      uint8_t* tp = sm.tpk(S) + 3 * c;
+      const uint8_t t = (uint8_t)(top > 0 ? top : 0);
+      wp[0] = (uint8_t)rgb; wp[1] = (uint8_t)(rgb >> 8); wp[2] = (uint8_t)(rgb >> 16);
+      tp[0] = t; tp[1] = t; tp[2] = t;
+    } else {
+      sm.wrgb(S)[wslot(c)] = rgb;
+      sm.t0(S)[c] = (uint16_t)(top > 0 ? top : 0);
+      sm.t8(S)[c] = (uint8_t)(top > 0 ? top : 0);
+      sm.b0(S)[c] = (uint16_t)(bot < H ? bot : H);
+    }
   };
   int c = lane;
   if (!CHECKED) {
@@ -1297,11 +1314,13 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
 // frame (h2 rows, contiguous in HBM) is cut into 16-byte chunks and lane l
 // of the group writes chunks l, l+G, l+2G, ... so every store instruction
 // covers G x 16 contiguous bytes (2 cache lines for 16 lanes instead of ~8
-// with the per-column layout) and the mirror row's chunk at the same row
+// with a per-column layout), plus the mirror row's chunk at the same row
 // offset. Needs CPR = 3W/16 chunks per row to divide 3G: then a lane's chunk
-// column repeats with period 3 (phases p) and its rows step by RB = 3G/CPR.
-// A chunk's 4 words span two quads qa, qa+1; one PRMT per word (selectors
-// precomputed per phase) turns the two SWAR row tests into the word's mask.
+// column k repeats with period 3 (phases p) and its rows step by RB = 3G/CPR.
+// The wall pass left the wall colours and tops as byte streams laid out like
+// a frame row (wpk / tpk), so chunk k's wall words and per-byte tops are one
+// 16-byte load each; per row and word: one SWAR subtract, one PRMT
+// sign-fill, one LOP3 each for the ceiling (top) and floor (bottom) blend.
 template <int NC, int G>
 __device__ __forceinline__ void mirror_contig(const SpecDev& S, const WarpSmem& sm, int m,
                                               uint8_t* __restrict__ frame) {
@@ -1311,44 +1330,41 @@ __device__ __forceinline__ void mirror_contig(const SpecDev& S, const WarpSmem& 
   const int row_bytes = W * 3;
   const int CPR = row_bytes >> 4;
   const int RB = 3 * G / CPR;
+  const uint4* __restrict__ wpk = reinterpret_cast<const uint4*>(sm.wpk(S));
+  const uint4* __restrict__ tpk = reinterpret_cast<const uint4*>(sm.tpk(S));
+  // ceiling / floor words by position of the word's first byte in its pixel
+  // (a chunk starting at byte 16k begins at component k mod 3)
   const uint32_t C = S.ceil_rgb, F = S.floor_rgb;
-  const uint32_t* __restrict__ t8w = reinterpret_cast<const uint32_t*>(sm.t8(S));
-  const uint32_t* __restrict__ wc = sm.wrgb(S);
+  const uint32_t c0 = __byte_perm(C, 0, 0x0210), c1 = __byte_perm(C, 0, 0x1021),
+                 c2 = __byte_perm(C, 0, 0x2102);
+  const uint32_t f0 = __byte_perm(F, 0, 0x0210), f1 = __byte_perm(F, 0, 0x1021),
+                 f2 = __byte_perm(F, 0, 0x2102);
 #pragma unroll 1
   for (int p = 0; p < 3; p++) {
     const int c = lane + G * p;
     const int rp = c / CPR, k = c - rp * CPR;
-    const int qa = (4 * k) / 3;
-    const uint32_t Ta = t8w[qa], Tb = t8w[qa + 1];
-    uint32_t Wd[4], sel[4], cw[4], fw[4];
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int wi = 4 * k + j;      // word index in the row
-      const int q = wi / 3, s = wi - 3 * q;
-      const uint32_t bp = s == 0 ? 0x4210u : (s == 1 ? 0x5421u : 0x6542u);
-      Wd[j] = __byte_perm(wc[wslot(4 * q + s)], wc[wslot(4 * q + s + 1)], bp);
-      cw[j] = __byte_perm(C, C, bp);
-      fw[j] = __byte_perm(F, F, bp);
-      const uint32_t ms = s == 0 ? 0x9888u : (s == 1 ? 0xAA99u : 0xBBBAu);
-      sel[j] = q == qa ? ms : ms + 0x4444u;  // second quad -> bytes 4..7
-    }
-    uint8_t* top = frame + (size_t)rp * row_bytes + 16 * k;
-    uint8_t* bot = frame + (size_t)(H - 1 - rp) * row_bytes + 16 * k;
-    const size_t step = (size_t)RB * row_bytes;
+    const int s0 = k % 3;
+    const uint4 Wd = wpk[k], T = tpk[k];
+    const uint32_t ca = s0 == 0 ? c0 : (s0 == 1 ? c1 : c2);
+    const uint32_t cb = s0 == 0 ? c1 : (s0 == 1 ? c2 : c0);
+    const uint32_t cc = s0 == 0 ? c2 : (s0 == 1 ? c0 : c1);
+    const uint32_t fa = s0 == 0 ? f0 : (s0 == 1 ? f1 : f2);
+    const uint32_t fb = s0 == 0 ? f1 : (s0 == 1 ? f2 : f0);
+    const uint32_t fc = s0 == 0 ? f2 : (s0 == 1 ? f0 : f1);
+    uint4* top = reinterpret_cast<uint4*>(frame + (size_t)rp * row_bytes) + k;
+    uint4* bot = reinterpret_cast<uint4*>(frame + (size_t)(H - 1 - rp) * row_bytes) + k;
+    const int step = RB * CPR;  // in uint4
+    const int nt = (h2 - rp + RB - 1) / RB;
 #pragma unroll 2
-    for (int r = rp; r < h2; r += RB, top += step, bot -= step) {
-      const uint32_t R = 0x80808080u + (uint32_t)r * 0x01010101u;
-      const uint32_t Da = R - Ta, Db = R - Tb;
-      uint32_t tw[4], bw[4];
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        uint32_t mk;
-        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(mk) : "r"(Da), "r"(Db), "r"(sel[j]));
-        tw[j] = (mk & Wd[j]) | (~mk & cw[j]);
-        bw[j] = (mk & Wd[j]) | (~mk & fw[j]);
-      }
-      TC_STORE(reinterpret_cast<uint4*>(top), make_uint4(tw[0], tw[1], tw[2], tw[3]));
-      TC_STORE(reinterpret_cast<uint4*>(bot), make_uint4(bw[0], bw[1], bw[2], bw[3]));
+    for (int t = 0; t < nt; t++, top += step, bot -= step) {
+      const uint32_t R = 0x80808080u + (uint32_t)(rp + t * RB) * 0x01010101u;
+      // MSB of byte b set iff row >= top of its pixel; sign-fill -> mask
+      const uint32_t m0 = prmt_sx(R - T.x, 0xBA98), m1 = prmt_sx(R - T.y, 0xBA98),
+                     m2 = prmt_sx(R - T.z, 0xBA98), m3 = prmt_sx(R - T.w, 0xBA98);
+      TC_STORE(top, make_uint4((m0 & Wd.x) | (~m0 & ca), (m1 & Wd.y) | (~m1 & cb),
+                               (m2 & Wd.z) | (~m2 & cc), (m3 & Wd.w) | (~m3 & ca)));
+      TC_STORE(bot, make_uint4((m0 & Wd.x) | (~m0 & fa), (m1 & Wd.y) | (~m1 & fb),
+                               (m2 & Wd.z) | (~m2 & fc), (m3 & Wd.w) | (~m3 & fa)));
     }
   }
   if (m > 0) {
