@@ -740,6 +740,106 @@ __device__ __forceinline__ void march_n(const uint32_t* __restrict__ solid, uint
   }
 }
 
+// R rays in lockstep over the shared-memory stop codes (map staged in smem,
+// fewer than 32 doors, sealed rim): every ray keeps a running shared-memory
+// byte address instead of a cell index, steps under a predicate (one DSETP,
+// one predicated DADD per axis, one SEL + IADD on the address, one LDS, one
+// LOP3 stop test against ~dmask -- walls ~0u always intersect it because bit
+// 31 of dmask is clear with < 32 doors). The side of the last step is
+// recovered from the last address increment (|stepx| = 4 B, |dyi| = 4*mw B,
+// mw >= 2), the step count (debug taps only) from the cell displacement
+// (each x step moves mapx by stepx, each y step mapy by stepy). The adds are
+// the reference's, in its order (_pycore.py:66-80).
+struct FastRay {
+  double sdx, sdy, ddx, ddy;
+  uint32_t addr;   // shared byte address of the current cell's stop code
+  int incx, incy;  // byte increments of an x / y step
+  int last;        // increment of the last step
+};
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Two rays: the whole loop in PTX so the live flags stay predicates and the
+// axis choice predicates the adds (the C version compiles to compute-both +
+// FSEL and byte-sized live flags: ~43 instructions per iteration vs 20).
+__device__ __forceinline__ void march_fast2(uint32_t smask, FastRay& a, FastRay& b) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred l0, l1, x0, y0, x1, y1, any;\n\t"
+      ".reg .b32 c0, c1, ix0, iy0, ix1, iy1, sm;\n\t"
+      ".reg .f64 ex0, ey0, ex1, ey1;\n\t"
+      // copy every input first: an input may share a register with an
+      // in/out operand (no early-clobber), and the loop writes those
+      "mov.f64 ex0, %8;\n\t"
+      "mov.f64 ey0, %9;\n\t"
+      "mov.b32 ix0, %10;\n\t"
+      "mov.b32 iy0, %11;\n\t"
+      "mov.f64 ex1, %12;\n\t"
+      "mov.f64 ey1, %13;\n\t"
+      "mov.b32 ix1, %14;\n\t"
+      "mov.b32 iy1, %15;\n\t"
+      "mov.b32 sm, %16;\n\t"
+      "setp.eq.b32 l0, sm, sm;\n\t"
+      "setp.eq.b32 l1, sm, sm;\n\t"
+      "MARCH%=:\n\t"
+      "setp.lt.and.f64 x0, %0, %1, l0;\n\t"
+      "setp.geu.and.f64 y0, %0, %1, l0;\n\t"
+      "setp.lt.and.f64 x1, %4, %5, l1;\n\t"
+      "setp.geu.and.f64 y1, %4, %5, l1;\n\t"
+      "@x0 add.rn.f64 %0, %0, ex0;\n\t"
+      "@y0 add.rn.f64 %1, %1, ey0;\n\t"
+      "@x1 add.rn.f64 %4, %4, ex1;\n\t"
+      "@y1 add.rn.f64 %5, %5, ey1;\n\t"
+      "@l0 selp.b32 %3, ix0, iy0, x0;\n\t"
+      "@l1 selp.b32 %7, ix1, iy1, x1;\n\t"
+      "@l0 add.u32 %2, %2, %3;\n\t"
+      "@l1 add.u32 %6, %6, %7;\n\t"
+      "@l0 ld.shared.u32 c0, [%2];\n\t"
+      "@l1 ld.shared.u32 c1, [%6];\n\t"
+      "@l0 and.b32 c0, c0, sm;\n\t"
+      "@l1 and.b32 c1, c1, sm;\n\t"
+      "@l0 setp.eq.b32 l0, c0, 0;\n\t"
+      "@l1 setp.eq.b32 l1, c1, 0;\n\t"
+      "or.pred any, l0, l1;\n\t"
+      "@any bra MARCH%=;\n\t"
+      "}"
+      : "+d"(a.sdx), "+d"(a.sdy), "+r"(a.addr), "+r"(a.last),
+        "+d"(b.sdx), "+d"(b.sdy), "+r"(b.addr), "+r"(b.last)
+      : "d"(a.ddx), "d"(a.ddy), "r"(a.incx), "r"(a.incy),
+        "d"(b.ddx), "d"(b.ddy), "r"(b.incx), "r"(b.incy), "r"(smask));
+}
+
+template <int R>
+__device__ __forceinline__ void march_fast(uint32_t smask, FastRay (&a)[R]) {
+  if constexpr (R == 2) {
+    march_fast2(smask, a[0], a[1]);
+    return;
+  }
+  uint32_t live = (1u << R) - 1u;
+#pragma unroll 1
+  do {
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      if (live & (1u << q)) {
+        const bool x = a[q].sdx < a[q].sdy;  // ties step Y (_pycore.py:70)
+        if (x) a[q].sdx += a[q].ddx; else a[q].sdy += a[q].ddy;
+        a[q].last = x ? a[q].incx : a[q].incy;
+        a[q].addr += a[q].last;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; q++) {
+      if (live & (1u << q)) {
+        if ((lds_u32(a[q].addr) & smask) != 0u) live &= ~(1u << q);
+      }
+    }
+  } while (live);
+}
+
 // Wall pass: lane L casts the rays of columns L + 32j; per-column spans,
 // colours and zbuf go to shared memory (_pycore.py:153-190). Returns the
 // status of the first failing column (warp-uniform).
@@ -795,7 +895,41 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     }
   };
   int c = lane;
-  if (!CHECKED) {
+  if (!CHECKED && S.smem_map && S.n_doors < 32 && mw >= 2) {
+    // shared-memory stop codes, predicated lockstep march (march_fast)
+    constexpr int LR = TC_LOCKSTEP;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(solid);
+    const uint32_t smask = ~e.dmask;
+    const int idx0 = oy * mw + ox;
+#pragma unroll 1
+    for (; c + (LR - 1) * G < W; c += LR * G) {
+      FastRay fr[LR];
+#pragma unroll
+      for (int q = 0; q < LR; q++) {
+        const double k = S.coef[c + q * G];
+        const RaySetup rs = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k, e.dy + planey * k);
+        fr[q].sdx = rs.sdx; fr[q].sdy = rs.sdy; fr[q].ddx = rs.ddx; fr[q].ddy = rs.ddy;
+        fr[q].addr = sbase + 4u * (uint32_t)idx0;
+        fr[q].incx = 4 * rs.stepx; fr[q].incy = 4 * rs.dyi;
+        fr[q].last = fr[q].incx;
+      }
+      march_fast<LR>(smask, fr);
+#pragma unroll
+      for (int q = 0; q < LR; q++) {
+        March r;
+        r.sdx = fr[q].sdx; r.sdy = fr[q].sdy; r.ddx = fr[q].ddx; r.ddy = fr[q].ddy;
+        r.idx = (int)(fr[q].addr - sbase) >> 2;
+        r.xs = fr[q].last == fr[q].incx;
+        r.status = TC_ST_OK;
+        r.steps = 0;
+        if (rayinfo) {
+          const int my = r.idx / mw, mx = r.idx - my * mw;
+          r.steps = abs(mx - ox) + abs(my - oy);
+        }
+        column_out(c + q * G, r);
+      }
+    }
+  } else if (!CHECKED) {
     // groups of TC_LOCKSTEP columns (c, c + G, ...) marched in lockstep
     constexpr int LR = TC_LOCKSTEP;
 #pragma unroll 1
