@@ -407,7 +407,10 @@ def main():
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 9,
                     "api": "batch_step_host(numpy actions, reuse=True) -> numpy rewards,"
-                           " dones (H2D + fused step + D2H + sync per step)",
+                           " dones per step: actions copied into pinned host memory and"
+                           " read by the step kernel over the bus (H2D), rewards + dones"
+                           " written back to pinned host memory by the kernel (D2H),"
+                           " stream sync, numpy copies out",
                     "episode_stats": stats},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

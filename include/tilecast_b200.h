@@ -178,6 +178,25 @@ int tc_batch_step_host(const tc_spec *spec, const tc_state *state_in,
                        tc_counters *counters_dev, double *rewards_host,
                        uint8_t *dones_host, void *stream);
 
+/* batch_step over HOST buffers with no copy engine on the path: the
+ * fused step kernel reads actions_host (i64[n]) straight from pinned host
+ * memory, and its last CTA writes [rewards f64[n] | dones u8[n]] (9n bytes,
+ * the out->rewards / out->dones device layout, 16-byte aligned) to
+ * results_host with coalesced 16-byte stores, then raises flag_host[1]; the
+ * call returns once flag_host[1] is set (the host spins on it instead of
+ * synchronising the stream, which still sees the kernel's teardown). flag_host
+ * is int32[2]: a contract-violating action sets flag_host[0] = 1 (the caller
+ * zeroes it before the call; flag_host[1] is managed by the call) and leaves that env's state unchanged in state_out, so
+ * the caller can raise the reference's ContractError (batch.py:92-106) with
+ * state_in still valid. Same semantics as tc_batch_step_host otherwise. All
+ * three host buffers must be page-locked and UVA-mapped (cudaHostAlloc /
+ * torch pin_memory), else TC_E_INVALID. */
+int tc_batch_step_mapped(const tc_spec *spec, const tc_state *state_in,
+                         const tc_state *state_out, const int64_t *actions_host,
+                         const tc_out *out, int64_t n, int32_t auto_reset,
+                         int32_t validate, tc_counters *counters_dev,
+                         uint8_t *results_host, int32_t *flag_host, void *stream);
+
 /* K fused steps in one launch with on-device uniform-random actions drawn
  * exactly as batch.policy_actions (batch.py:141-153) would draw them for
  * steps [step0, step0+K) of an (n_total)-env rollout whose env 0 is global

@@ -90,6 +90,8 @@ def _load() -> C.CDLL:
                                          C.c_int32, C.c_int32, _p, _p]),
         "tc_batch_step_host": (C.c_int, [_p, P(TcState), P(TcState), _p, _p, P(TcOut), C.c_int64,
                                          C.c_int32, C.c_int32, _p, _p, _p, _p]),
+        "tc_batch_step_mapped": (C.c_int, [_p, P(TcState), P(TcState), _p, P(TcOut), C.c_int64,
+                                           C.c_int32, C.c_int32, _p, _p, _p, _p]),
         "tc_rollout": (C.c_int, [_p, P(TcState), P(TcOut), C.c_int64, C.c_int64, C.c_int64,
                                  C.c_uint64, C.c_int64, C.c_int32, C.c_int32, _p, _p]),
         "tc_seed_streams": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, _p, _p, _p]),

@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <atomic>
 #include <vector>
 
 #include "../../include/tilecast_b200.h"
@@ -141,6 +142,10 @@ struct OutDev {
   int32_t* statuses;
   int32_t* rayinfo;
   unsigned long long* spritevis;
+  // mapped host step (tc_batch_step_mapped): the last CTA copies
+  // [rewards f64[n] | dones u8[n]] to res_host; a bad action sets *flag_host
+  uint8_t* res_host;
+  int32_t* flag_host;
 };
 
 struct RolloutArgs {
@@ -1729,7 +1734,9 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   // prologue as our CTAs retire, and stage the (constant) map before
   // waiting for the previous step's state to be complete and visible
   asm volatile("griddepcontrol.launch_dependents;");
-  if ((long long)blockIdx.x >= n) return;  // no env for this CTA (n < grid)
+  // no env for this CTA (n < grid); it still counts itself done when the
+  // last CTA ships the results to the host
+  if ((long long)blockIdx.x >= n && !out.res_host) return;
   stage_map(S, smap, cell, solid);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
@@ -1766,6 +1773,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
         TRACE(i, 1);
         if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
           status = TC_ST_BAD_ACTION;
+          if (out.flag_host && lane == 0) *(volatile int32_t*)out.flag_host = 1;
           store_env<G>(S, so, i, e);  // out-of-place: carry the state over
         } else {
           const StepOut o = step_dynamics(S, cell, solid, e, (int)act, validate);
@@ -1809,14 +1817,36 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       if (badbits) atomicOr(&counters->bad_status, badbits);
     }
   }
-  if (dyn) {
+  if (dyn || out.res_host) {
+    // every warp is done with its shared memory: word 0 carries the flag
+    volatile int& s_last = *reinterpret_cast<int*>(smem);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      if (atomicAdd(&counters->ctas_done, 1u) == gridDim.x - 1) {
+      const bool last = atomicAdd(&counters->ctas_done, 1u) == gridDim.x - 1;
+      if (last) {
         counters->next_env = 0;
         counters->ctas_done = 0;
       }
+      s_last = last;
+    }
+    __syncthreads();
+    if (s_last && out.res_host) {
+      // every CTA's rewards / dones are visible (fence before the count);
+      // ship them to pinned host memory with 16-byte coalesced stores
+      __threadfence();
+      const size_t bytes = (size_t)n * 9, nv = bytes >> 4;
+      const uint4* src = reinterpret_cast<const uint4*>(out.rewards);
+      uint4* dst = reinterpret_cast<uint4*>(out.res_host);
+      for (size_t k = threadIdx.x; k < nv; k += blockDim.x) dst[k] = __ldcg(src + k);
+      const uint8_t* sb = reinterpret_cast<const uint8_t*>(out.rewards);
+      for (size_t k = nv * 16 + threadIdx.x; k < bytes; k += blockDim.x)
+        out.res_host[k] = __ldcg(sb + k);
+      // results (and every CTA's state / frame writes) are complete: raise
+      // the host's completion word once the copies are visible system-wide
+      __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x == 0) *(volatile int32_t*)(out.flag_host + 1) = 1;
     }
   }
 }
@@ -2149,6 +2179,8 @@ OutDev to_dev(const tc_out* o) {
   d.truncs = o->truncs; d.events = o->events; d.statuses = o->statuses;
   d.rayinfo = o->rayinfo;
   d.spritevis = reinterpret_cast<unsigned long long*>(o->spritevis);
+  d.res_host = nullptr;
+  d.flag_host = nullptr;
   return d;
 }
 
@@ -2274,7 +2306,8 @@ int tc_spec_destroy(tc_spec* s) {
 static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc_state* state_out,
                                const int64_t* actions_dev, const tc_out* out, int64_t n,
                                int32_t mode, int32_t auto_reset, int32_t validate,
-                               tc_counters* counters_dev, void* stream) {
+                               tc_counters* counters_dev, void* stream,
+                               uint8_t* res_host = nullptr, int32_t* flag_host = nullptr) {
   if (!s || !state || !out) return fail(TC_E_INVALID, "NULL spec/state/out");
   if (n < 0) return fail(TC_E_INVALID, "n must be >= 0");
   if (mode != TC_MODE_RESET && mode != TC_MODE_STEP && mode != MODE_RENDER)
@@ -2290,6 +2323,8 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
   StateDev sd = to_dev(state);
   StateDev so = to_dev(state_out ? state_out : state);
   OutDev od = to_dev(out);
+  od.res_host = res_host;
+  od.flag_host = flag_host;
   const int grid = grid_for(s, n);
   const long long nn = n;
   const long long* acts = reinterpret_cast<const long long*>(actions_dev);
@@ -2353,6 +2388,60 @@ int tc_batch_step_host(const tc_spec* s, const tc_state* state_in, const tc_stat
       TC_CUDA(cudaMemcpyAsync(dones_host, out->dones, (size_t)n, cudaMemcpyDeviceToHost, st));
   }
   TC_CUDA(cudaStreamSynchronize(st));
+  return TC_OK;
+}
+
+int tc_batch_step_mapped(const tc_spec* s, const tc_state* state_in, const tc_state* state_out,
+                         const int64_t* actions_host, const tc_out* out, int64_t n,
+                         int32_t auto_reset, int32_t validate, tc_counters* counters_dev,
+                         uint8_t* results_host, int32_t* flag_host, void* stream) {
+  if (!actions_host || !results_host || !flag_host || !counters_dev)
+    return fail(TC_E_INVALID, "NULL actions / results / flag / counters");
+  if (!state_out) return fail(TC_E_INVALID, "state_out is NULL");
+  if (n <= 0) return n == 0 ? TC_OK : fail(TC_E_INVALID, "n must be >= 0");
+  if (!out || reinterpret_cast<uint8_t*>(out->rewards) + (size_t)n * 8 != out->dones)
+    return fail(TC_E_INVALID, "out->dones must follow out->rewards ([rewards | dones])");
+  if ((reinterpret_cast<uintptr_t>(out->rewards) | reinterpret_cast<uintptr_t>(results_host)) & 15u)
+    return fail(TC_E_INVALID, "rewards / results_host must be 16-byte aligned");
+  // the device reads / writes these host buffers directly: they must be
+  // page-locked and mapped into the device's address space (UVA)
+  // (checked once per buffer triple: a step loop reuses the same buffers)
+  static thread_local const void* checked[3] = {nullptr, nullptr, nullptr};
+  if (checked[0] != actions_host || checked[1] != results_host || checked[2] != flag_host) {
+    for (const void* p : {(const void*)actions_host, (const void*)results_host,
+                          (const void*)flag_host}) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeHost ||
+          a.devicePointer != p) {
+        cudaGetLastError();
+        return fail(TC_E_INVALID, "host buffers must be pinned and UVA-mapped");
+      }
+    }
+    checked[0] = actions_host; checked[1] = results_host; checked[2] = flag_host;
+  }
+  volatile int32_t* done = flag_host + 1;
+  *done = 0;
+  const int rc = launch_batch_kernel(s, state_in, state_out, actions_host, out, n, TC_MODE_STEP,
+                                     auto_reset, validate, counters_dev, stream, results_host,
+                                     flag_host);
+  if (rc != TC_OK) return rc;
+  // the last CTA raises *done after the results reached host memory: spin
+  // on it (the kernel's teardown and the stream's completion need not be
+  // waited for); poll the stream now and then so a faulting kernel surfaces
+  for (unsigned spin = 1; *done == 0; spin++) {
+    if ((spin & 1023u) == 0) {
+      const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+      if (q == cudaSuccess) {
+        if (*done == 0) return fail(TC_E_CUDA, "step kernel finished without results");
+        break;
+      }
+      if (q != cudaErrorNotReady) {
+        cudaGetLastError();
+        return fail(TC_E_CUDA, cudaGetErrorString(q));
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   return TC_OK;
 }
 

@@ -279,6 +279,32 @@ def test_batch_step_host_matches_device_path():
         assert np.array_equal(ha[k], hb[k]), k
     with pytest.raises(tc.ContractError):
         tc.batch_step_host(b, [int(tc.Action.STRAFE_LEFT)] * n)
+    bad = acts[0].copy()
+    bad[n // 2] = 99
+    with pytest.raises(tc.ContractError):
+        tc.batch_step_host(b, bad)
+    bad[n // 2] = -1
+    with pytest.raises(tc.ContractError):
+        tc.batch_step_host(b, bad)
+    # a rejected step leaves the state usable and unchanged
+    a, ra, da = tc.batch_step(a, acts[1], reuse=True)
+    b, rb, db = tc.batch_step_host(b, acts[1], reuse=True)
+    assert np.array_equal(ra.cpu().numpy(), rb) and torch.equal(a.frames, b.frames)
+    b.check()
+
+
+@pytest.mark.parametrize("n", [1, 5, 37])
+def test_batch_step_host_small_batches(n):
+    # fewer envs than CTAs: idle CTAs still take part in the result hand-off
+    spec = tc.make_env("dmlab-random-goal-01", max_steps=12)
+    acts = tc.policy_actions(spec, n, 30, 4)
+    a = tc.batch_reset(spec, n, 4, device=DEV)
+    b = tc.batch_reset(spec, n, 4, device=DEV)
+    for s in range(30):
+        a, ra, da = tc.batch_step(a, acts[s], reuse=True)
+        b, rb, db = tc.batch_step_host(b, acts[s], reuse=True)
+        assert np.array_equal(ra.cpu().numpy(), rb) and np.array_equal(da.cpu().numpy(), db)
+    assert torch.equal(a.frames, b.frames)
 
 
 def test_gym_vecenv_and_env_match_core():

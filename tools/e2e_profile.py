@@ -72,6 +72,15 @@ for s in range(K):
     lib.tc_batch_step_host(*args2)
 t1 = time.perf_counter()
 print(f"raw C call without D2H {1e6*(t1-t0)/K:.1f} us")
+args3 = (bs._ds.handle, N.C.byref(bs._sb.c_struct()), N.C.byref(sb.c_struct()), stg.h_act_ptr,
+         N.C.byref(ob.c_struct()), bs.n, 1, 0, N.ptr(bs._counters), stg.h_rew_ptr,
+         stg.h_flag_ptr, stream_ptr(bs.device))
+t0 = time.perf_counter()
+for s in range(K):
+    lib.tc_batch_step_mapped(*args3)
+t1 = time.perf_counter()
+print(f"raw mapped C call (kernel reads actions / writes results over the bus + sync) "
+      f"{1e6*(t1-t0)/K:.1f} us")
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
