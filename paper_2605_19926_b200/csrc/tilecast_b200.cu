@@ -33,6 +33,7 @@
 #include <mutex>
 #include <string>
 #include <atomic>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/tilecast_b200.h"
@@ -818,8 +819,101 @@ __device__ __forceinline__ void march_fast2(uint32_t smask, FastRay& a, FastRay&
         "d"(b.ddx), "d"(b.ddy), "r"(b.incx), "r"(b.incy), "r"(smask));
 }
 
+// Four rays in lockstep (TC_LOCKSTEP=4): same loop as march_fast2; each
+// ray's x / y byte increments arrive packed as (incy << 8) | (incx & 0xff)
+// to stay within the asm operand limit.
+__device__ __forceinline__ void march_fast4(uint32_t smask, FastRay (&a)[4]) {
+  uint32_t pk[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) pk[q] = ((uint32_t)a[q].incy << 8) | ((uint32_t)a[q].incx & 0xffu);
+  asm volatile(
+      "{\n\t"
+      ".reg .pred l0, l1, l2, l3, x0, y0, x1, y1, x2, y2, x3, y3, any;\n\t"
+      ".reg .b32 c0, c1, c2, c3, ix0, iy0, ix1, iy1, ix2, iy2, ix3, iy3, sm, t;\n\t"
+      ".reg .f64 ex0, ey0, ex1, ey1, ex2, ey2, ex3, ey3;\n\t"
+      // inputs are copied first (no early-clobber on the in/out operands)
+      "mov.f64 ex0, %16;\n\t"
+      "mov.f64 ey0, %17;\n\t"
+      "shl.b32 t, %18, 24;\n\t"
+      "shr.s32 ix0, t, 24;\n\t"
+      "shr.s32 iy0, %18, 8;\n\t"
+      "mov.f64 ex1, %19;\n\t"
+      "mov.f64 ey1, %20;\n\t"
+      "shl.b32 t, %21, 24;\n\t"
+      "shr.s32 ix1, t, 24;\n\t"
+      "shr.s32 iy1, %21, 8;\n\t"
+      "mov.f64 ex2, %22;\n\t"
+      "mov.f64 ey2, %23;\n\t"
+      "shl.b32 t, %24, 24;\n\t"
+      "shr.s32 ix2, t, 24;\n\t"
+      "shr.s32 iy2, %24, 8;\n\t"
+      "mov.f64 ex3, %25;\n\t"
+      "mov.f64 ey3, %26;\n\t"
+      "shl.b32 t, %27, 24;\n\t"
+      "shr.s32 ix3, t, 24;\n\t"
+      "shr.s32 iy3, %27, 8;\n\t"
+      "mov.b32 sm, %28;\n\t"
+      "setp.eq.b32 l0, sm, sm;\n\t"
+      "setp.eq.b32 l1, sm, sm;\n\t"
+      "setp.eq.b32 l2, sm, sm;\n\t"
+      "setp.eq.b32 l3, sm, sm;\n\t"
+      "MARCH4%=:\n\t"
+      "setp.lt.and.f64 x0, %0, %1, l0;\n\t"
+      "setp.geu.and.f64 y0, %0, %1, l0;\n\t"
+      "setp.lt.and.f64 x1, %4, %5, l1;\n\t"
+      "setp.geu.and.f64 y1, %4, %5, l1;\n\t"
+      "setp.lt.and.f64 x2, %8, %9, l2;\n\t"
+      "setp.geu.and.f64 y2, %8, %9, l2;\n\t"
+      "setp.lt.and.f64 x3, %12, %13, l3;\n\t"
+      "setp.geu.and.f64 y3, %12, %13, l3;\n\t"
+      "@x0 add.rn.f64 %0, %0, ex0;\n\t"
+      "@y0 add.rn.f64 %1, %1, ey0;\n\t"
+      "@x1 add.rn.f64 %4, %4, ex1;\n\t"
+      "@y1 add.rn.f64 %5, %5, ey1;\n\t"
+      "@x2 add.rn.f64 %8, %8, ex2;\n\t"
+      "@y2 add.rn.f64 %9, %9, ey2;\n\t"
+      "@x3 add.rn.f64 %12, %12, ex3;\n\t"
+      "@y3 add.rn.f64 %13, %13, ey3;\n\t"
+      "@l0 selp.b32 %3, ix0, iy0, x0;\n\t"
+      "@l0 add.u32 %2, %2, %3;\n\t"
+      "@l1 selp.b32 %7, ix1, iy1, x1;\n\t"
+      "@l1 add.u32 %6, %6, %7;\n\t"
+      "@l2 selp.b32 %11, ix2, iy2, x2;\n\t"
+      "@l2 add.u32 %10, %10, %11;\n\t"
+      "@l3 selp.b32 %15, ix3, iy3, x3;\n\t"
+      "@l3 add.u32 %14, %14, %15;\n\t"
+      "@l0 ld.shared.u32 c0, [%2];\n\t"
+      "@l1 ld.shared.u32 c1, [%6];\n\t"
+      "@l2 ld.shared.u32 c2, [%10];\n\t"
+      "@l3 ld.shared.u32 c3, [%14];\n\t"
+      "@l0 and.b32 c0, c0, sm;\n\t"
+      "@l0 setp.eq.b32 l0, c0, 0;\n\t"
+      "@l1 and.b32 c1, c1, sm;\n\t"
+      "@l1 setp.eq.b32 l1, c1, 0;\n\t"
+      "@l2 and.b32 c2, c2, sm;\n\t"
+      "@l2 setp.eq.b32 l2, c2, 0;\n\t"
+      "@l3 and.b32 c3, c3, sm;\n\t"
+      "@l3 setp.eq.b32 l3, c3, 0;\n\t"
+      "or.pred any, l0, l1;\n\t"
+      "or.pred any, any, l2;\n\t"
+      "or.pred any, any, l3;\n\t"
+      "@any bra MARCH4%=;\n\t"
+      "}"
+      : "+d"(a[0].sdx), "+d"(a[0].sdy), "+r"(a[0].addr), "+r"(a[0].last),
+        "+d"(a[1].sdx), "+d"(a[1].sdy), "+r"(a[1].addr), "+r"(a[1].last),
+        "+d"(a[2].sdx), "+d"(a[2].sdy), "+r"(a[2].addr), "+r"(a[2].last),
+        "+d"(a[3].sdx), "+d"(a[3].sdy), "+r"(a[3].addr), "+r"(a[3].last)
+      : "d"(a[0].ddx), "d"(a[0].ddy), "r"(pk[0]), "d"(a[1].ddx), "d"(a[1].ddy), "r"(pk[1]),
+        "d"(a[2].ddx), "d"(a[2].ddy), "r"(pk[2]), "d"(a[3].ddx), "d"(a[3].ddy), "r"(pk[3]),
+        "r"(smask));
+}
+
 template <int R>
 __device__ __forceinline__ void march_fast(uint32_t smask, FastRay (&a)[R]) {
+  if constexpr (R == 4) {
+    march_fast4(smask, a);
+    return;
+  }
   if constexpr (R == 2) {
     march_fast2(smask, a[0], a[1]);
     return;
@@ -901,13 +995,13 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
   };
   int c = lane;
   if (!CHECKED && S.smem_map && S.n_doors < 32 && mw >= 2) {
-    // shared-memory stop codes, predicated lockstep march (march_fast)
-    constexpr int LR = TC_LOCKSTEP;
+    // shared-memory stop codes, predicated lockstep march (march_fast):
+    // rounds of TC_LOCKSTEP columns (c, c + G, ...), then pairs, then singles
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(solid);
     const uint32_t smask = ~e.dmask;
     const int idx0 = oy * mw + ox;
-#pragma unroll 1
-    for (; c + (LR - 1) * G < W; c += LR * G) {
+    auto fast_round = [&](auto rtag) {
+      constexpr int LR = decltype(rtag)::value;
       FastRay fr[LR];
 #pragma unroll
       for (int q = 0; q < LR; q++) {
@@ -933,6 +1027,13 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
         }
         column_out(c + q * G, r);
       }
+    };
+    constexpr int LR = TC_LOCKSTEP;
+#pragma unroll 1
+    for (; c + (LR - 1) * G < W; c += LR * G) fast_round(std::integral_constant<int, LR>());
+    if (LR > 2) {
+#pragma unroll 1
+      for (; c + G < W; c += 2 * G) fast_round(std::integral_constant<int, 2>());
     }
   } else if (!CHECKED) {
     // groups of TC_LOCKSTEP columns (c, c + G, ...) marched in lockstep
@@ -1692,7 +1793,18 @@ __device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, 
     st.ealive[i * S.n_ent + k] = (uint8_t)((e.emask >> k) & 1ULL);
 }
 
-// packed cells + stop codes into shared memory once per CTA
+// packed cells + stop codes into shared memory once per CTA: [cells,
+// padded to 4 words | stop codes with their wall guards, padded to 4 words],
+// copied as 16-byte cp.async chunks (all in flight at once; the blob's
+// entries are 16-byte aligned and padded, so the rounded-up tail reads stay
+// inside it)
+__host__ __device__ __forceinline__ int map_words_cells(int h, int w) { return (h * w + 3) & ~3; }
+__host__ __device__ __forceinline__ int map_words_solid(int h, int w) {
+  return (h * w + 2 * (w + 1) + 3) & ~3;
+}
+__host__ __device__ __forceinline__ int map_smem_bytes(const SpecDev& S) {
+  return S.smem_map ? 4 * (map_words_cells(S.h, S.w) + map_words_solid(S.h, S.w)) : 0;
+}
 __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, const uint32_t*& cell,
                                           const uint32_t*& solid) {
   if (!S.smem_map) {
@@ -1700,14 +1812,19 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
     solid = S.solid;
     return;
   }
-  const int cells = S.h * S.w, guard = S.w + 1;
-  for (int k = threadIdx.x; k < cells; k += blockDim.x) smap[k] = S.cell[k];
-  // stop codes with their wall guards: [guard | cells | guard]
-  const uint32_t* gsrc = S.solid - guard;
-  for (int k = threadIdx.x; k < cells + 2 * guard; k += blockDim.x) smap[cells + k] = gsrc[k];
+  const int guard = S.w + 1;
+  const int wc = map_words_cells(S.h, S.w), ws = map_words_solid(S.h, S.w);
+  const int n4c = wc >> 2, n4 = (wc + ws) >> 2;
+  const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(smap);
+  for (int k = threadIdx.x; k < n4; k += blockDim.x) {
+    const uint32_t* src = k < n4c ? S.cell + 4 * k : (S.solid - guard) + 4 * (k - n4c);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16u * k), "l"(src)
+                 : "memory");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   cell = smap;
-  solid = smap + cells + guard;
+  solid = smap + wc + guard;
 }
 
 
@@ -1728,7 +1845,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   const int lane = g.lane;
   const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;  // group id in the CTA
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
-  const int map_bytes = S.smem_map ? align16((S.h * S.w * 2 + 2 * (S.w + 1)) * 4) : 0;
+  const int map_bytes = map_smem_bytes(S);
   const uint32_t *cell, *solid;
   // programmatic dependent launch: let the next step's grid start its
   // prologue as our CTAs retire, and stage the (constant) map before
@@ -1864,7 +1981,7 @@ rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateD
   const int lane = g.lane;
   const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
-  const int map_bytes = S.smem_map ? align16((S.h * S.w * 2 + 2 * (S.w + 1)) * 4) : 0;
+  const int map_bytes = map_smem_bytes(S);
   const uint32_t *cell, *solid;
   if ((long long)blockIdx.x >= n) return;  // no env for this CTA (n < grid)
   stage_map(S, smap, cell, solid);
@@ -2140,7 +2257,7 @@ int launch_geometry(tc_spec* s) {
   if (d.npairs > 4) d.npairs = 4;
   d.warp_smem = warp_smem_layout(d, d.direct == 1 ? 0 : (d.mirror ? 2 * d.npairs : 2));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
-  const size_t map_bytes = d.smem_map ? (size_t)align16((d.h * d.w * 2 + 2 * (d.w + 1)) * 4) : 0;
+  const size_t map_bytes = (size_t)map_smem_bytes(d);
   s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * (32 / d.group) * d.warp_smem;
   s->nc = pick_nc(d.obs_w, d.group);
   const void* fns[2] = {select_batch(s->nc, d.group), select_rollout(s->nc, d.group)};
