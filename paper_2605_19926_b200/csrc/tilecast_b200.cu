@@ -344,7 +344,7 @@ __device__ __noinline__ uint64_t scan_tiles(const SpecDev& S, const uint32_t* __
 }
 
 // _pycore.py:390-414: draws in the contract order spawn, heading, goal
-__device__ __forceinline__ void reset_draws(const SpecDev& S, Env& e) {
+__device__ __forceinline__ void reset_draws_inl(const SpecDev& S, Env& e) {
   unsigned long long ctr = e.rctr;
   uint64_t v = draw_below(e.rkey, ctr, (uint64_t)S.n_spawns);
   e.x = S.spx[v];
@@ -367,6 +367,19 @@ __device__ __forceinline__ void reset_draws(const SpecDev& S, Env& e) {
   e.done = 0;
   e.dmask = 0;
   e.emask = S.n_ent >= 64 ? ~0ULL : ((1ULL << S.n_ent) - 1ULL);
+}
+
+// out of line: runs once per episode (instruction-cache footprint)
+__device__ __noinline__ Env reset_env(const SpecDev& S, unsigned long long rkey,
+                                      unsigned long long rctr) {
+  Env e;
+  e.rkey = rkey;
+  e.rctr = rctr;
+  reset_draws_inl(S, e);
+  return e;
+}
+__device__ __forceinline__ void reset_draws(const SpecDev& S, Env& e) {
+  e = reset_env(S, e.rkey, e.rctr);
 }
 
 struct StepOut {
@@ -948,7 +961,7 @@ __device__ __forceinline__ void march_fast(uint32_t smask, FastRay (&a)[R]) {
 // Wall pass: lane L casts the rays of columns L + 32j; per-column spans,
 // colours and zbuf go to shared memory (_pycore.py:153-190). Returns the
 // status of the first failing column (warp-uniform).
-template <int NC, bool CHECKED, int G>
+template <int NC, bool CHECKED, int G, bool FAST = false>
 __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __restrict__ cell,
                                          const uint32_t* __restrict__ solid,
                                          const WarpSmem& sm, const Env& e, double planex,
@@ -1000,7 +1013,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     }
   };
   int c = lane;
-  if (!CHECKED && S.smem_map && S.n_doors < 32 && mw >= 2) {
+  if (FAST || (!CHECKED && S.smem_map && S.n_doors < 32 && mw >= 2)) {
     // shared-memory stop codes, predicated lockstep march (march_fast):
     // rounds of TC_LOCKSTEP columns (c, c + G, ...), then pairs, then singles
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(solid);
@@ -1041,7 +1054,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
 #pragma unroll 1
       for (; c + G < W; c += 2 * G) fast_round(std::integral_constant<int, 2>());
     }
-  } else if (!CHECKED) {
+  } else if (!CHECKED && !FAST) {
     // groups of TC_LOCKSTEP columns (c, c + G, ...) marched in lockstep
     constexpr int LR = TC_LOCKSTEP;
 #pragma unroll 1
@@ -1340,6 +1353,19 @@ __device__ __forceinline__ void put_quad(uint32_t* dst, uint32_t p0, uint32_t p1
 }
 
 // Render one environment's frame (all 32 lanes of the warp participate).
+// the wall pass for maps / poses off the fast path (unsealed rim, origin
+// off the grid, global-memory stop codes, 32 doors)
+template <int NC, int G>
+__device__ __noinline__ int wall_pass_cold(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                           const uint32_t* __restrict__ solid, WarpSmem sm,
+                                           Env e, double planex, double planey,
+                                           double* __restrict__ zbuf_out,
+                                           int32_t* __restrict__ rayinfo, bool sealed_inside) {
+  return sealed_inside
+      ? wall_pass<NC, false, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
+      : wall_pass<NC, true, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo);
+}
+
 // Returns the status of the first failing column (or OK), warp-uniform.
 // _pycore.py:132-271.
 // Phase 1 of rendering: wall pass (spans / zbuf into shared memory).
@@ -1351,11 +1377,14 @@ __device__ __forceinline__ int render_walls(const SpecDev& S, const uint32_t* __
                                             int32_t* __restrict__ rayinfo) {
   const double planex = -e.dy * PLANE_HALF_WIDTH;
   const double planey = e.dx * PLANE_HALF_WIDTH;
-  // fast march when the rim is sealed and the origin is on the grid
+  // fast march when the rim is sealed, the origin is on the grid and the
+  // stop codes sit in shared memory; every other case runs out of line so
+  // the hot kernel body stays compact (instruction-cache footprint)
   const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h;
-  const int st = (S.sealed && inside)
-      ? wall_pass<NC, false, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
-      : wall_pass<NC, true, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo);
+  const int st = (S.sealed && inside && S.smem_map && S.n_doors < 32 && S.w >= 2)
+      ? wall_pass<NC, false, G, true>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
+      : wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo,
+                              S.sealed && inside);
   Grp<G>().sync();
   return st;
 }
@@ -1622,9 +1651,40 @@ __device__ __forceinline__ void mirror_contig(const SpecDev& S, const WarpSmem& 
 
 // Phase 3: compose the frame in staged bands, draw sprites, ship with TMA.
 template <int NC, int G>
+__device__ __forceinline__ void render_frame_general(const SpecDev& S, const WarpSmem& sm, int m,
+                                                     uint8_t* __restrict__ frame,
+                                                     int& bulk_pending, int& buf,
+                                                     const LaneGeo& lg);
+
+// bulk_pending | buf << 16 (no references across the out-of-line call)
+template <int NC, int G>
+__device__ __noinline__ int render_frame_cold(const SpecDev& S, WarpSmem sm, int m,
+                                              uint8_t* __restrict__ frame, int bulk_pending,
+                                              int buf, LaneGeo lg) {
+  render_frame_general<NC, G>(S, sm, m, frame, bulk_pending, buf, lg);
+  return bulk_pending | (buf << 16);
+}
+
+template <int NC, int G>
 __device__ __forceinline__ void render_frame_out(const SpecDev& S, const WarpSmem& sm, int m,
                                                  uint8_t* __restrict__ frame, int& bulk_pending,
                                                  int& buf, const LaneGeo& lg) {
+  // the lane-contiguous direct compose inline; every other layout out of
+  // line (instruction-cache footprint of the hot kernel)
+  if (S.mirror && S.direct == 1 && S.contig) {
+    mirror_contig<NC, G>(S, sm, m, frame);
+    return;
+  }
+  const int r = render_frame_cold<NC, G>(S, sm, m, frame, bulk_pending, buf, lg);
+  bulk_pending = r & 0xffff;
+  buf = r >> 16;
+}
+
+template <int NC, int G>
+__device__ __forceinline__ void render_frame_general(const SpecDev& S, const WarpSmem& sm, int m,
+                                                     uint8_t* __restrict__ frame,
+                                                     int& bulk_pending, int& buf,
+                                                     const LaneGeo& lg) {
   const Grp<G> g;
   const int lane = g.lane;
   const int W = S.obs_w, H = S.obs_h;
