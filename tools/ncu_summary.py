@@ -54,6 +54,9 @@ keys = {
     "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "lsu_pipe_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
     "sm_clock_hz": "smsp__cycles_elapsed.avg.per_second",
+    "icache_hit_pct": "sm__icc_request_hit_rate.pct",
+    "local_ld_inst": "smsp__sass_inst_executed_op_local_ld.sum",
+    "local_st_inst": "smsp__sass_inst_executed_op_local_st.sum",
 }
 res = {k: (d.get(v) if k == "kernel" else f(v)) for k, v in keys.items()}
 stalls = {}
