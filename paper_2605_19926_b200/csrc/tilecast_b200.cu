@@ -79,6 +79,7 @@ constexpr int WARPS_PER_CTA = 4;
 #define TC_MIN_CTAS 5  // resident CTAs per SM the register budget is sized for
 #endif
 constexpr int BAND_BYTES_TARGET = 3072;       // per staging buffer
+constexpr int CTA_SCRATCH = 160;               // step kernel per-CTA scratch bytes
 constexpr int SMEM_MAP_MAX_CELLS = 4096;      // stage map in smem up to this
 
 // packed cell word: bits 0-7 = wall colour or door index, 8-9 = cell tag,
@@ -1319,9 +1320,14 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
               mk = (x & 3) ? 1 : ((x & 4) ? 2 : 0);
             }
             if (mk) {
+              // a pixel is 3 bytes: one aligned 16-bit store + one byte store
+              // (bytes 0-1 + 2 at an even address, byte 0 + bytes 1-2 at an
+              // odd one; every lane runs the same two stores)
               const uint32_t col = mk == 1 ? r.s1 : r.s2;
               uint8_t* d = drow + (lane + G * j) * 3;
-              d[0] = (uint8_t)col; d[1] = (uint8_t)(col >> 8); d[2] = (uint8_t)(col >> 16);
+              const int odd = (int)(reinterpret_cast<uintptr_t>(d) & 1u);
+              *reinterpret_cast<uint16_t*>(d + odd) = (uint16_t)(col >> (8 * odd));
+              d[odd ? 0 : 2] = (uint8_t)(odd ? col : col >> 16);
             }
           }
         }
@@ -1871,8 +1877,8 @@ __host__ __device__ __forceinline__ int map_words_solid(int h, int w) {
 __host__ __device__ __forceinline__ int map_smem_bytes(const SpecDev& S) {
   return S.smem_map ? 4 * (map_words_cells(S.h, S.w) + map_words_solid(S.h, S.w)) : 0;
 }
-__device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, const uint32_t*& cell,
-                                          const uint32_t*& solid) {
+__device__ __forceinline__ void stage_map_issue(const SpecDev& S, uint32_t* smap,
+                                                const uint32_t*& cell, const uint32_t*& solid) {
   if (!S.smem_map) {
     cell = S.cell;
     solid = S.solid;
@@ -1887,10 +1893,17 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16u * k), "l"(src)
                  : "memory");
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
   cell = smap;
   solid = smap + wc + guard;
+}
+__device__ __forceinline__ void stage_map_wait() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+}
+__device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, const uint32_t*& cell,
+                                          const uint32_t*& solid) {
+  stage_map_issue(S, smap, cell, solid);
+  stage_map_wait();
 }
 
 
@@ -1919,8 +1932,48 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   asm volatile("griddepcontrol.launch_dependents;");
   // no env for this CTA (n < grid); it still counts itself done when the
   // last CTA ships the results to the host
-  if ((long long)blockIdx.x >= n && !out.res_host) return;
-  stage_map(S, smap, cell, solid);
+  // env scheduling. One wave (n <= groups in the grid): CTA c owns the
+  // contiguous envs [c*epc, c*epc + epc), epc = ceil(n / grid) <= groups per
+  // CTA, so every SM gets the same number of envs +-1 and a CTA's actions /
+  // results are one contiguous run (one bus transaction each on the mapped
+  // host path). Several waves: env grp*grid + cta first, then envs pulled
+  // from a self-resetting device ticket counter (the last CTA to finish
+  // zeroes it for the next launch).
+  const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
+  const bool dyn = counters != nullptr && n > stride;
+  const int epc = dyn ? 0 : (int)((n + gridDim.x - 1) / gridDim.x);
+  const long long cbase = (long long)blockIdx.x * epc;
+  const int cta_envs = dyn ? 0 : (int)max(0LL, min((long long)epc, n - cbase));
+  // no env for this CTA; it still counts itself done on the mapped host path
+  if ((dyn ? (long long)blockIdx.x >= n : cta_envs == 0) && !out.res_host) return;
+  const long long i_first = dyn ? (long long)grp * gridDim.x + blockIdx.x
+                                : (grp < cta_envs ? cbase + grp : n);
+  // per-CTA scratch after the group windows: actions / rewards / dones of
+  // the CTA's envs (one-wave mapping)
+  uint8_t* cta_s = smem + map_bytes + WARPS_PER_CTA * NG * S.warp_smem;
+  long long* act_s = reinterpret_cast<long long*>(cta_s);
+  double* rew_s = reinterpret_cast<double*>(cta_s + 64);
+  uint8_t* done_s = cta_s + 128;
+  // the actions are loaded before the map staging and the dependent-launch
+  // wait so their latency (HBM, or the host bus on the mapped host path)
+  // overlaps them; actions are inputs, never written by the preceding step
+  // kernel
+  const bool warp0 = threadIdx.x < 32;
+  long long a_pre = 0;
+  if (mode == MODE_STEP) {
+    if (!dyn) {
+      if (warp0 && (int)threadIdx.x < cta_envs) a_pre = actions[cbase + threadIdx.x];
+    } else if (i_first < n) {
+      a_pre = actions[i_first];
+    }
+  }
+  stage_map_issue(S, smap, cell, solid);
+  if (!dyn && warp0 && (int)threadIdx.x < cta_envs) {
+    act_s[threadIdx.x] = a_pre;
+    rew_s[threadIdx.x] = 0.0;
+    done_s[threadIdx.x] = 0;
+  }
+  stage_map_wait();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
@@ -1928,15 +1981,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   int bulk_pending = 0, buf = 0;
   unsigned long long viol = 0;
   uint32_t badbits = 0;
-  // env scheduling: env i0 = global group id first; envs beyond one wave are
-  // pulled dynamically from a device ticket counter (self-resetting: the
-  // last CTA to finish zeroes it for the next launch)
-  const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
-  const bool dyn = counters != nullptr && n > stride;
-  // first env of each group: interleaved over CTAs (env = grp * grid + cta)
-  // so a partial wave spreads evenly over the SMs instead of filling the
-  // first CTAs
-  long long i = (long long)grp * gridDim.x + blockIdx.x;
+  long long i = i_first;
   while (i < n) {
     // grab the next ticket now; its latency hides behind this env's work
     long long tnext = i + stride;
@@ -1952,7 +1997,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     } else {
       load_env<G>(S, st, i, e);
       if (mode == MODE_STEP) {
-        const long long act = actions[i];
+        const long long act = i != i_first ? actions[i] : (dyn ? a_pre : act_s[grp]);
         TRACE(i, 1);
         if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
           status = TC_ST_BAD_ACTION;
@@ -1965,6 +2010,10 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
             out.dones[i] = (uint8_t)o.done;
             out.truncs[i] = (uint8_t)o.trunc;
             out.events[i] = o.events;
+            if (!dyn && out.res_host) {
+              rew_s[grp] = o.reward;
+              done_s[grp] = (uint8_t)o.done;
+            }
           }
           viol += (unsigned long long)o.violation;
           if (o.done && auto_reset) reset_draws(S, e);
@@ -2004,6 +2053,18 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     // every warp is done with its shared memory: word 0 carries the flag
     volatile int& s_last = *reinterpret_cast<int*>(smem);
     __syncthreads();
+    if (!dyn && out.res_host) {
+      // one-wave mapping: the CTA's contiguous rewards / dones go to pinned
+      // host memory as one run each, made visible system-wide before the CTA
+      // counts itself done (a voided bad-action env keeps reward 0, done 0)
+      if (warp0 && (int)threadIdx.x < cta_envs) {
+        const int k = threadIdx.x;
+        reinterpret_cast<double*>(out.res_host)[cbase + k] = rew_s[k];
+        out.res_host[(size_t)n * 8 + cbase + k] = done_s[k];
+        __threadfence_system();
+      }
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
       __threadfence();
       const bool last = atomicAdd(&counters->ctas_done, 1u) == gridDim.x - 1;
@@ -2014,7 +2075,13 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       s_last = last;
     }
     __syncthreads();
-    if (s_last && out.res_host) {
+    if (s_last && out.res_host && !dyn) {
+      // every CTA's results reached host memory before it was counted
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        *(volatile int32_t*)(out.flag_host + 1) = 1;
+      }
+    } else if (s_last && out.res_host) {
       // every CTA's rewards / dones are visible (fence before the count);
       // ship them to pinned host memory with 16-byte coalesced stores
       __threadfence();
@@ -2340,7 +2407,8 @@ int launch_geometry(tc_spec* s) {
   d.warp_smem = warp_smem_layout(d, d.direct == 1 ? 0 : (d.mirror ? 2 * d.npairs : 2));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
   const size_t map_bytes = (size_t)map_smem_bytes(d);
-  s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * (32 / d.group) * d.warp_smem;
+  // + the per-CTA scratch of the step kernel (actions / rewards / dones)
+  s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * (32 / d.group) * d.warp_smem + CTA_SCRATCH;
   s->nc = pick_nc(d.obs_w, d.group);
   const void* fns[3] = {select_batch(s->nc, d.group), select_rollout(s->nc, d.group),
                         select_batch(s->nc, d.group, true)};
