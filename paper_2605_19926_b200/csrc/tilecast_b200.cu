@@ -299,49 +299,93 @@ __device__ __forceinline__ RayHit cast_ray(const uint32_t* __restrict__ cell, in
 }
 
 
+// A group of G lanes (G = 32: one env per warp; G = 16: two envs per warp,
+// one per half) and its collectives. Masks are the group's own, so the two
+// halves of a warp may diverge freely.
+template <int G>
+struct Grp {
+  int lane;        // lane within the group
+  int shift;       // bit offset of the group inside the warp
+  unsigned mask;   // member mask
+  __device__ __forceinline__ Grp() {
+    const int l = threadIdx.x & 31;
+    lane = l & (G - 1);
+    shift = l & ~(G - 1) & 31;
+    mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << shift);
+  }
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    return (__ballot_sync(mask, p) & mask) >> shift;
+  }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  template <class T>
+  __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src, G); }
+  __device__ __forceinline__ int min(int v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = ::min(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+  }
+  __device__ __forceinline__ int max(int v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = ::max(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+  }
+};
+
 // One pass over the <= 2x2 tiles the disc (cx, cy, radius) overlaps, doing
 // _touch_doors (_pycore.py:307-343; only when `touch`) and then _blocked
 // (:274-304) for each tile. Equivalent to the reference's two passes: a
 // door's open flag only affects its own tile (one door record per door
-// cell), and touch never skips a tile that blocked would test. Returns the
-// door events; result packs (door mask, events, blocked-after-touch).
-__device__ __noinline__ uint64_t scan_tiles(const SpecDev& S, const uint32_t* __restrict__ cell,
-                                            const uint32_t* __restrict__ solid, uint32_t dmask,
-                                            double cx, double cy, double radius, uint32_t inv,
-                                            bool touch) {
-  uint32_t events = 0;
-  bool b = false;
+// cell), and touch never skips a tile that blocked would test. The tiles are
+// tested lane-parallel (lane q of the group takes tile (tx0 + q%2, ty0 +
+// q/2)) and combined with group reductions. Returns (door mask, events,
+// blocked-after-touch) packed.
+template <int G>
+__device__ __forceinline__ uint64_t scan_tiles(const SpecDev& S, const uint32_t* __restrict__ cell,
+                                               const uint32_t* __restrict__ solid,
+                                               uint32_t dmask, double cx, double cy,
+                                               double radius, uint32_t inv, bool touch) {
+  const Grp<G> g;
   const int tx0 = (int)floor(cx - radius), tx1 = (int)floor(cx + radius);
   const int ty0 = (int)floor(cy - radius), ty1 = (int)floor(cy + radius);
   const double r2 = radius * radius;
-#pragma unroll 1
-  for (int ty = ty0; ty <= ty1; ty++) {
-#pragma unroll 1
-    for (int tx = tx0; tx <= tx1; tx++) {
-      if (tx < 0 || tx >= S.w || ty < 0 || ty >= S.h) { b = true; continue; }
+  const int tx = tx0 + (g.lane & 1), ty = ty0 + ((g.lane >> 1) & 1);
+  uint32_t opened = 0, events = 0;
+  bool b = false;
+  if (g.lane < 4 && tx <= tx1 && ty <= ty1) {
+    if (tx < 0 || tx >= S.w || ty < 0 || ty >= S.h) {
+      b = true;
+    } else {
       const uint32_t code = solid[ty * S.w + tx];
-      if (code == 0u) continue;  // floor
-      double nx = cx;
-      if (nx < tx) nx = tx;
-      else if (nx > tx + 1.0) nx = tx + 1.0;
-      double ny = cy;
-      if (ny < ty) ny = ty;
-      else if (ny > ty + 1.0) ny = ty + 1.0;
-      const double ddx = cx - nx, ddy = cy - ny;
-      if (!(ddx * ddx + ddy * ddy < r2)) continue;  // no overlap
-      if (code != 0xffffffffu && (code & ~dmask) != 0u && touch) {  // closed door
-        const int di = (int)(cell[ty * S.w + tx] & 31u);
-        const int dc = S.dcol[di];
-        if (!(S.dlock[di] != 0 && ((inv >> dc) & 1u) == 0)) {
-          dmask |= 1u << di;
-          events |= 1u << (EV_DOOR_BASE_BIT + dc);
+      if (code != 0u) {  // not floor
+        double nx = cx;
+        if (nx < tx) nx = tx;
+        else if (nx > tx + 1.0) nx = tx + 1.0;
+        double ny = cy;
+        if (ny < ty) ny = ty;
+        else if (ny > ty + 1.0) ny = ty + 1.0;
+        const double ddx = cx - nx, ddy = cy - ny;
+        if (ddx * ddx + ddy * ddy < r2) {  // overlap
+          uint32_t dm = dmask;
+          if (code != 0xffffffffu && (code & ~dm) != 0u && touch) {  // closed door
+            const int di = (int)(cell[ty * S.w + tx] & 31u);
+            const int dc = S.dcol[di];
+            if (!(S.dlock[di] != 0 && ((inv >> dc) & 1u) == 0)) {
+              opened = 1u << di;
+              events = 1u << (EV_DOOR_BASE_BIT + dc);
+              dm |= opened;
+            }
+          }
+          if ((code & ~dm) != 0u || code == 0xffffffffu) b = true;
         }
       }
-      if ((code & ~dmask) != 0u || code == 0xffffffffu) b = true;
     }
   }
+  dmask |= __reduce_or_sync(g.mask, opened);
+  events = __reduce_or_sync(g.mask, events);
+  const bool blk = g.any(b);
   // packed result: new door mask | events << 32 | blocked << 63
-  return (uint64_t)dmask | ((uint64_t)events << 32) | ((uint64_t)(b ? 1 : 0) << 63);
+  return (uint64_t)dmask | ((uint64_t)events << 32) | ((uint64_t)(blk ? 1 : 0) << 63);
 }
 
 // _pycore.py:390-414: draws in the contract order spawn, heading, goal
@@ -389,7 +433,9 @@ struct StepOut {
   int done, trunc, violation;
 };
 
-// _pycore.py:431-531 (everything before the render / auto-reset branch)
+// _pycore.py:431-531 (everything before the render / auto-reset branch);
+// called by all G lanes of the group (the tile scan is lane-parallel)
+template <int G>
 __device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_t* __restrict__ cell,
                                                  const uint32_t* __restrict__ solid, Env& e,
                                                  int act, int validate) {
@@ -420,7 +466,7 @@ __device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_
       if (ax == 2 && !validate) break;
       const double cx = ax == 0 ? x + mvx : x;
       const double cy = ax == 1 ? y + mvy : y;
-      const uint64_t r = scan_tiles(S, cell, solid, e.dmask, cx, cy, radius, e.inv, ax < 2);
+      const uint64_t r = scan_tiles<G>(S, cell, solid, e.dmask, cx, cy, radius, e.inv, ax < 2);
       e.dmask = (uint32_t)r;
       o.events |= (uint32_t)(r >> 32) & 0x3ffu;
       const bool blk = (r >> 63) != 0;
@@ -567,38 +613,6 @@ __device__ inline WarpSmem carve(uint8_t* base) {
   return m;
 }
 
-// A group of G lanes (G = 32: one env per warp; G = 16: two envs per warp,
-// one per half) and its collectives. Masks are the group's own, so the two
-// halves of a warp may diverge freely.
-template <int G>
-struct Grp {
-  int lane;        // lane within the group
-  int shift;       // bit offset of the group inside the warp
-  unsigned mask;   // member mask
-  __device__ __forceinline__ Grp() {
-    const int l = threadIdx.x & 31;
-    lane = l & (G - 1);
-    shift = l & ~(G - 1) & 31;
-    mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << shift);
-  }
-  __device__ __forceinline__ unsigned ballot(bool p) const {
-    return (__ballot_sync(mask, p) & mask) >> shift;
-  }
-  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
-  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
-  template <class T>
-  __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src, G); }
-  __device__ __forceinline__ int min(int v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v = ::min(v, __shfl_xor_sync(mask, v, o, G));
-    return v;
-  }
-  __device__ __forceinline__ int max(int v) const {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v = ::max(v, __shfl_xor_sync(mask, v, o, G));
-    return v;
-  }
-};
 
 // One DDA march, _pycore.py:38-96. `solid` holds per-cell stop codes
 // (wall = ~0u, door d = 1u << d, floor = 0): a ray stops in a cell iff
@@ -2004,7 +2018,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
           if (out.flag_host && lane == 0) *(volatile int32_t*)out.flag_host = 1;
           store_env<G>(S, so, i, e);  // out-of-place: carry the state over
         } else {
-          const StepOut o = step_dynamics(S, cell, solid, e, (int)act, validate);
+          const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
           if (lane == 0) {
             out.rewards[i] = o.reward;
             out.dones[i] = (uint8_t)o.done;
@@ -2133,7 +2147,7 @@ rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateD
       const long long step = ra.step0 + k;
       unsigned long long ctr = (unsigned long long)(step * ra.n_total + ra.base + i);
       const int act = ra.tags[draw_below(ra.policy_key, ctr, (uint64_t)ra.n_tags)];
-      const StepOut o = step_dynamics(S, cell, solid, e, act, 0);
+      const StepOut o = step_dynamics<G>(S, cell, solid, e, act, 0);
       const size_t kn = (size_t)k * (size_t)n + (size_t)i;
       if (lane == 0) {
         if (out.rewards) out.rewards[kn] = o.reward;
@@ -2298,6 +2312,10 @@ int validate_tables(const tc_tables* t, std::vector<uint32_t>& cells,
   if (!t) return fail(TC_E_INVALID, "tables is NULL");
   if (t->h < 1 || t->w < 1) return fail(TC_E_INVALID, "empty map");
   if (t->obs_w < 8 || t->obs_h < 8) return fail(TC_E_INVALID, "observation must be at least 8x8");
+  // the lane-parallel collision scan covers a 2x2 tile box (radius 0.2 in
+  // every shipped spec, tables.py:19-31)
+  if (!(t->fc[FC_RADIUS] >= 0.0 && t->fc[FC_RADIUS] < 0.5))
+    return fail(TC_E_INVALID, "agent radius must be in [0, 0.5)");
   if (t->obs_w > TC_MAX_OBS_W || t->obs_h > TC_MAX_OBS_H)
     return fail(TC_E_CAPACITY, "observation larger than TC_MAX_OBS_W/H");
   if (t->n_entities < 0 || t->n_entities > TC_MAX_ENTITIES)
