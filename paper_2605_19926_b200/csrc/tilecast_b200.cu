@@ -126,6 +126,7 @@ struct SpecDev {
   int npairs;        // mirror path: staged band pairs in flight (2..4)
   int o_t0, o_b0, o_t8, o_wrgb, o_zbuf, o_gdep, o_recs, o_band;  // WarpSmem offsets
   int o_wpk, o_tpk;  // contig compose: packed wall RGB / per-byte top row streams
+  int o_sct;         // contig sprites: per-column terms (f64[W] then u8[W] flags)
   int warp_smem;     // bytes of per-warp shared memory
 };
 
@@ -571,6 +572,10 @@ struct WarpSmem {
   __device__ __forceinline__ uint32_t* wrgb(const SpecDev& S) const { return (uint32_t*)(base + S.o_wrgb); }
   __device__ __forceinline__ uint8_t* wpk(const SpecDev& S) const { return base + S.o_wpk; }
   __device__ __forceinline__ uint8_t* tpk(const SpecDev& S) const { return base + S.o_tpk; }
+  __device__ __forceinline__ double* sct(const SpecDev& S) const { return (double*)(base + S.o_sct); }
+  __device__ __forceinline__ uint8_t* scf(const SpecDev& S) const {
+    return base + S.o_sct + 8 * ((S.obs_w + 15) & ~15);
+  }
   __device__ __forceinline__ double* zbuf(const SpecDev& S) const { return (double*)(base + S.o_zbuf); }
   __device__ __forceinline__ double* gdep(const SpecDev& S) const { return (double*)(base + S.o_gdep); }
   __device__ __forceinline__ SpriteRec* recs(const SpecDev& S) const { return (SpriteRec*)(base + S.o_recs); }
@@ -604,6 +609,7 @@ __host__ inline int warp_smem_layout(SpecDev& d, int nbands) {
   // frame row (3 bytes per column)
   d.o_wpk = off; off += d.contig ? align16(3 * wp) : 0;
   d.o_tpk = off; off += d.contig ? align16(3 * wp) : 0;
+  d.o_sct = off; off += d.contig ? align16(9 * wp) : 0;
   return align16(off);
 }
 
@@ -1605,6 +1611,120 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
   g.sync();
 }
 
+// Sprites over a directly stored frame (contig compose): same terms and
+// comparisons as draw_sprites, but the lanes are remapped onto the sprite's
+// visible column span [lo, hi] (per-column terms go through shared memory),
+// so a sprite w columns wide costs ceil(w / G) column slots per row instead
+// of W / G. Pixels leave as one 16-bit + one 8-bit store.
+template <int NC, int G>
+__device__ __noinline__ void draw_sprites_direct(const SpecDev& S, WarpSmem sm, int m,
+                                                 uint8_t* __restrict__ frame) {
+  const Grp<G> g;
+  const int lane = g.lane;
+  const int W = S.obs_w, row_bytes = W * 3;
+  double* sct = sm.sct(S);
+  uint8_t* scf = sm.scf(S);
+  for (int s = 0; s < m; s++) {
+    const SpriteRec r = sm.recs(S)[s];
+    const double denom = (double)r.denom;
+    const bool key = r.kd == K_KEY;
+    // column terms of the lane's own columns -> shared memory; visible span
+    int lo = 0x7fffffff, hi = -1;
+#pragma unroll
+    for (int j = 0; j < NC; j++) {
+      const int c = lane + G * j;
+      if (c >= W) continue;
+      double ct = 0.0;
+      int cf = 0;
+      bool vis = false;
+      if (!(sm.zbuf(S)[c] <= r.dep)) {
+        const double a = (S.coef[c] - r.ks) / r.halfk;
+        if (!(a <= -1.0 || a >= 1.0)) {
+          vis = true;
+          const double aa = a >= 0.0 ? a : -a;
+          if (r.kd == K_GOAL) {
+            ct = aa;
+          } else if (key) {
+            const double ea = aa / 0.30;
+            ct = ea * ea;
+            cf = (aa <= 0.07 ? 1 : 0) | (aa <= 0.24 ? 6 : 0);
+          } else {
+            cf = (aa <= 0.10 ? 1 : 0) | (aa <= 0.38 ? 2 : 0) | (aa <= 0.60 ? 4 : 0);
+          }
+        }
+      }
+      sct[c] = ct;
+      scf[c] = (uint8_t)(vis ? (cf | 0x80) : 0);
+      if (vis) { lo = min(lo, c); hi = max(hi, c); }
+    }
+    lo = g.min(lo);
+    hi = g.max(hi);
+    if (hi < 0) continue;
+    g.sync();
+    const int ncv = (hi - lo + G) / G;  // column slots over [lo, hi]
+    double ct[NC];
+    int cf[NC];
+#pragma unroll
+    for (int j = 0; j < NC; j++) {
+      const int c = lo + lane + G * j;
+      const bool in = j < ncv && c <= hi;
+      ct[j] = in ? sct[c] : 0.0;
+      cf[j] = in ? scf[c] : 0;
+    }
+    const int ra = r.r0, rb = r.r1;
+    for (int r32 = ra; r32 < rb; r32 += G) {
+      // lane-parallel row terms (_pycore.py:99-129 split into factors)
+      double rt_l = 0.0;
+      int rf_l = 0;
+      if (r32 + lane < rb) {
+        const double v = ((double)(r32 + lane - r.vtop) + 0.5) / denom;
+        if (r.kd == K_GOAL) {
+          double dv = v - 0.5;
+          if (dv < 0.0) dv = -dv;
+          rt_l = dv * 2.0;
+        } else if (key) {
+          const double ev = (v - 0.30) / 0.18;
+          rt_l = ev * ev;
+          rf_l = (0.30 <= v && v <= 0.85 ? 1 : 0) | (0.62 <= v && v <= 0.70 ? 2 : 0) |
+                 (0.76 <= v && v <= 0.84 ? 4 : 0);
+        } else {
+          rf_l = (0.32 <= v && v <= 0.73 ? 1 : 0) | (0.47 <= v && v <= 0.60 ? 2 : 0) |
+                 (0.25 <= v && v <= 0.80 ? 4 : 0);
+        }
+      }
+      const int nr = min(G, rb - r32);
+      for (int k = 0; k < nr; k++) {
+        const double rt = g.shfl(rt_l, k);
+        const int rf = g.shfl(rf_l, k);
+        uint8_t* drow = frame + (size_t)(r32 + k) * row_bytes;
+#pragma unroll
+        for (int j = 0; j < NC; j++) {
+          if (j >= ncv) break;
+          if (!(cf[j] & 0x80)) continue;
+          int mk;
+          if (r.kd == K_GOAL) {
+            mk = (ct[j] + rt <= 0.8) ? 1 : 0;  // aa + |v-0.5|*2.0 <= 0.8
+          } else if (key) {
+            const double e = ct[j] + rt;        // ea*ea + ev*ev
+            mk = ((0.30 <= e && e <= 1.0) || (cf[j] & rf & 7) != 0) ? 1 : 0;
+          } else {
+            const int x = cf[j] & rf & 7;
+            mk = (x & 3) ? 1 : ((x & 4) ? 2 : 0);
+          }
+          if (mk) {
+            const uint32_t col = mk == 1 ? r.s1 : r.s2;
+            uint8_t* d = drow + (lo + lane + G * j) * 3;
+            const int odd = (int)(reinterpret_cast<uintptr_t>(d) & 1u);
+            *reinterpret_cast<uint16_t*>(d + odd) = (uint16_t)(col >> (8 * odd));
+            d[odd ? 0 : 2] = (uint8_t)(odd ? col : col >> 16);
+          }
+        }
+      }
+    }
+    g.sync();  // the next sprite reuses the column-term scratch
+  }
+}
+
 // Direct mirrored compose with lane-contiguous stores: the top half of the
 // frame (h2 rows, contiguous in HBM) is cut into 16-byte chunks and lane l
 // of the group writes chunks l, l+G, l+2G, ... so every store instruction
@@ -1664,7 +1784,7 @@ __device__ __forceinline__ void mirror_contig(const SpecDev& S, const WarpSmem& 
   }
   if (m > 0) {
     g.sync();
-    draw_sprites<NC, G>(S, sm, m, frame, 0, nullptr, 0, H);
+    draw_sprites_direct<NC, G>(S, sm, m, frame);
   }
   g.sync();
 }
