@@ -166,6 +166,20 @@ int tc_batch_step_into(const tc_spec *spec, const tc_state *state_in,
                        const tc_out *out, int64_t n, int32_t auto_reset,
                        int32_t validate, tc_counters *counters_dev, void *stream);
 
+/* Heterogeneous-map step (the reference steps one
+ * homogeneous batch per batch_kernel call, tables.py:251-273):
+ * n_groups out-of-place steps, group g = counts[g] envs of specs[g] with
+ * states_in[g] -> states_out[g], actions actions_dev[offset_g ..], outputs
+ * outs[g] (typically views of one batch-wide block), counters[g] (one per
+ * group). The groups run concurrently on library-owned side streams forked
+ * from and joined back into `stream`; the call is asynchronous like
+ * tc_batch_step_into. */
+int tc_multi_step(const tc_spec *const *specs, const tc_state *states_in,
+                  const tc_state *states_out, const int64_t *actions_dev,
+                  const tc_out *outs, const int64_t *counts, int32_t n_groups,
+                  int32_t auto_reset, int32_t validate, tc_counters *const *counters,
+                  void *stream);
+
 /* batch_step over HOST buffers in one call (batch.py:109-138 semantics, the
  * reference's numpy-in / numpy-out contract): H2D of actions_host into
  * actions_dev, one fused out-of-place step, D2H of rewards (f64[n]) and

@@ -2779,6 +2779,70 @@ int tc_batch_step_into(const tc_spec* s, const tc_state* state_in, const tc_stat
                              auto_reset, validate, counters_dev, stream);
 }
 
+int tc_multi_step(const tc_spec* const* specs, const tc_state* states_in,
+                  const tc_state* states_out, const int64_t* actions_dev, const tc_out* outs,
+                  const int64_t* counts, int32_t n_groups, int32_t auto_reset, int32_t validate,
+                  tc_counters* const* counters, void* stream) {
+  if (!specs || !states_in || !states_out || !actions_dev || !outs || !counts || !counters)
+    return fail(TC_E_INVALID, "NULL group array");
+  if (n_groups < 1) return fail(TC_E_INVALID, "n_groups must be >= 1");
+  for (int g = 0; g < n_groups; g++) {
+    if (!specs[g] || !counters[g]) return fail(TC_E_INVALID, "NULL spec / counters in a group");
+    if (counts[g] < 1) return fail(TC_E_INVALID, "every group needs >= 1 env");
+  }
+  // Groups run concurrently on side streams forked from / joined back into
+  // the caller's stream, so one group's tail overlaps the others' work (each
+  // group has its own counters: its env tickets are private).
+  constexpr int kSide = 4;
+  struct Side {
+    int dev = -1;
+    cudaStream_t st[kSide] = {};
+    cudaEvent_t fork = nullptr, join[kSide] = {};
+  };
+  static thread_local Side side;
+  int dev = 0;
+  TC_CUDA(cudaGetDevice(&dev));
+  if (side.dev != dev) {
+    // one lazily created set per thread and device in use (re-created on a
+    // device switch; the previous set is released)
+    if (side.dev >= 0) {
+      for (int k = 0; k < kSide; k++) {
+        cudaStreamDestroy(side.st[k]);
+        cudaEventDestroy(side.join[k]);
+      }
+      cudaEventDestroy(side.fork);
+    }
+    side.dev = -1;
+    TC_CUDA(cudaEventCreateWithFlags(&side.fork, cudaEventDisableTiming));
+    for (int k = 0; k < kSide; k++) {
+      TC_CUDA(cudaStreamCreateWithFlags(&side.st[k], cudaStreamNonBlocking));
+      TC_CUDA(cudaEventCreateWithFlags(&side.join[k], cudaEventDisableTiming));
+    }
+    side.dev = dev;
+  }
+  cudaStream_t main_st = (cudaStream_t)stream;
+  const int used = n_groups < kSide ? n_groups : kSide;
+  if (n_groups == 1) {
+    return launch_batch_kernel(specs[0], &states_in[0], &states_out[0], actions_dev, &outs[0],
+                               counts[0], TC_MODE_STEP, auto_reset, validate, counters[0], stream);
+  }
+  TC_CUDA(cudaEventRecord(side.fork, main_st));
+  for (int k = 0; k < used; k++) TC_CUDA(cudaStreamWaitEvent(side.st[k], side.fork, 0));
+  int64_t off = 0;
+  for (int g = 0; g < n_groups; g++) {
+    const int rc = launch_batch_kernel(specs[g], &states_in[g], &states_out[g], actions_dev + off,
+                                       &outs[g], counts[g], TC_MODE_STEP, auto_reset, validate,
+                                       counters[g], side.st[g % kSide]);
+    if (rc != TC_OK) return rc;
+    off += counts[g];
+  }
+  for (int k = 0; k < used; k++) {
+    TC_CUDA(cudaEventRecord(side.join[k], side.st[k]));
+    TC_CUDA(cudaStreamWaitEvent(main_st, side.join[k], 0));
+  }
+  return TC_OK;
+}
+
 int tc_batch_step_host(const tc_spec* s, const tc_state* state_in, const tc_state* state_out,
                        const int64_t* actions_host, int64_t* actions_dev, const tc_out* out,
                        int64_t n, int32_t auto_reset, int32_t validate,

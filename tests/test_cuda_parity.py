@@ -340,3 +340,77 @@ def test_cli_bench_report_schema():
     assert set(rep["results"]) >= {"steps_per_second", "frames_per_second", "us_per_frame",
                                    "reward_sum"}
     assert rep["results"]["steps_per_second"] > 0
+
+
+@pytest.mark.parametrize("env,n,m", [("my-way-home", 4096, 300), ("key-door", 2048, 1)])
+def test_back_to_back_steps_without_sync(env, n, m):
+    """Consecutive one-wave step launches overlap (per-CTA launch chain,
+    csrc batch_kernel): K steps of two batches on the same spec and stream,
+    actions pre-staged on the device, no host read in between -- the final
+    state, frames and last outputs equal the oracle's."""
+    spec = tc.make_env(env, max_steps=23)
+    k = 40
+    runs = []
+    for nn, seed in ((n, 3), (m, 4)):
+        acts = tc.policy_actions(spec, nn, k, seed)
+        runs.append((tc.batch_reset(spec, nn, seed, device=DEV),
+                     torch.from_numpy(acts).to(DEV), orc.Rollout(spec, nn, seed), acts))
+    torch.cuda.synchronize()
+    states = [r[0] for r in runs]
+    outs = [None, None]
+    for s in range(k):
+        for j, (_, acts_dev, _, _) in enumerate(runs):
+            states[j], rew, done = tc.batch_step(states[j], acts_dev[s], reuse=True,
+                                                 copy_outputs=False)
+            outs[j] = (rew, done)
+    torch.cuda.synchronize()
+    for j, (_, _, r, acts) in enumerate(runs):
+        for s in range(k):
+            r.step(acts[s])
+        bs = states[j]
+        assert np.array_equal(outs[j][0].cpu().numpy(), r.out["rewards"]), j
+        assert np.array_equal(outs[j][1].cpu().numpy(), r.out["dones"] != 0), j
+        assert np.array_equal(bs.frames.cpu().numpy(), r.out["frames"]), j
+        _assert_state(bs, r.state, f"batch {j}")
+        bs.check()
+
+
+def test_multimap_batch_matches_per_group_oracle():
+    """Heterogeneous maps (multimap.py): groups over different specs (a
+    synthetic map, key-door with doors / sprites, my-way-home) share one
+    output block; group g equals the oracle's homogeneous run with base =
+    its offset, whether stepped with numpy or device actions."""
+    syn = tc.EnvSpec(id="syn-mm", map=random_tilemap(random.Random(77)),
+                     action_set=tc.suite.STRAFE_ACTIONS,
+                     goal_mode=tc.GoalMode.RANDOM_PER_EPISODE, max_steps=19,
+                     living_reward=0.01, health_decay=1.0, health_restore=10.0)
+    specs = [syn, tc.make_env("key-door", max_steps=31), tc.make_env("my-way-home", max_steps=27)]
+    counts = [700, 129, 1500]
+    seed, k = 9, 45
+    mb = tc.multi_reset(specs, counts, seed, device=DEV)
+    n = sum(counts)
+    assert mb.frames.shape == (n, 64, 64, 3)
+    refs, acts = [], []
+    for spec, c, off in zip(specs, counts, mb.offsets):
+        refs.append(orc.Rollout(spec, c, seed, base=off))
+        acts.append(tc.policy_actions(spec, c, k, seed + off))
+    assert np.array_equal(mb.frames.cpu().numpy(),
+                          np.concatenate([r.out["frames"] for r in refs])), "reset frames"
+    full = np.concatenate(acts, axis=1)
+    full_dev = torch.from_numpy(full).to(DEV)
+    for s in range(k):
+        a = full[s] if s % 2 == 0 else full_dev[s]
+        mb, rew, done = tc.multi_step(mb, a, reuse=True)
+        for r, ac in zip(refs, acts):
+            r.step(ac[s])
+        if s % 7 == 0 or s == k - 1:
+            assert np.array_equal(rew.cpu().numpy(),
+                                  np.concatenate([r.out["rewards"] for r in refs])), s
+            assert np.array_equal(done.cpu().numpy(),
+                                  np.concatenate([r.out["dones"] != 0 for r in refs])), s
+            assert np.array_equal(mb.frames.cpu().numpy(),
+                                  np.concatenate([r.out["frames"] for r in refs])), s
+            for g, r in zip(mb.groups, refs):
+                _assert_state(g, r.state, f"step {s} group {g.spec.id}")
+    mb.check()
+    assert mb.group_of(0) == 0 and mb.group_of(700) == 1 and mb.group_of(n - 1) == 2

@@ -94,3 +94,16 @@ def test_event_tags_and_actions():
     assert tc.event_tags((1 << 0) | (1 << 9)) == ("picked_key_red", "truncated")
     assert tc.ACTIONS_BY_NAME["noop"] == tc.Action.NOOP
     assert len(tc.suite.NAV_ACTIONS) == 5 and len(tc.suite.STRAFE_ACTIONS) == 7
+
+
+def test_multimap_contracts():
+    """Heterogeneous-map batches check their groups on the host before any
+    device work (multimap.py)."""
+    a = tc.make_env("my-way-home")
+    b = tc.make_env("key-door", obs_width=32, obs_height=32)
+    with pytest.raises(tc.ContractError, match="observation shape"):
+        tc.multi_reset([a, b], [4, 4], seed=0)
+    with pytest.raises(tc.ContractError, match=">= 1 env"):
+        tc.multi_reset([a, a], [4, 0], seed=0)
+    with pytest.raises(tc.ContractError, match="equal length"):
+        tc.multi_reset([a], [4, 4], seed=0)
