@@ -3,8 +3,9 @@
     python tools/bench_multimap.py [--maps 16] [--envs 131072] [--steps 50]
 
 Synthetic random tile maps (conftest.random_tilemap semantics, 64x64 obs):
-the same N envs once as one homogeneous batch (map 0) and once split over
---maps different maps (one step launch per map group per step, one output
+the same N envs as one homogeneous batch (map 0), as one homogeneous
+batch on each map in turn (weighted by the group sizes: the maps' own
+cost), and split over --maps different maps (one step launch per map group per step, one output
 block). Actions pre-staged on the device; CUDA events on the launching
 stream; frames (N x 12 KB) exceed L2. Prints one JSON line.
 """
@@ -71,6 +72,18 @@ def main():
     ms_h = timed(step_homo, args.steps, args.warmup)
     ms_m = timed(step_multi, args.steps, args.warmup)
     homo[0].check()
+    # the same N envs homogeneously on each map in turn: the cost of the maps
+    # themselves (random maps differ in size and ray length), without the split
+    ms_each = []
+    for k in range(m):
+        one = [tc.batch_reset(specs[k], n, 0, device=dev)]
+
+        def step_one(s, one=one):
+            one[0], _, _ = tc.batch_step(one[0], acts[s], reuse=True, copy_outputs=False)
+
+        ms_each.append(timed(step_one, max(10, args.steps // 4), args.warmup))
+        one[0].check()
+    ms_mix = sum(ms_each[k] * counts[k] / n for k in range(m))
     mm[0].check()
     print(json.dumps({
         "metric": "env steps/sec (rendered frames/sec)", "unit": "env-steps/s",
@@ -78,7 +91,9 @@ def main():
         "homogeneous": {"value": n / (ms_h * 1e-3), "ms_per_step": ms_h},
         "heterogeneous": {"value": n / (ms_m * 1e-3), "ms_per_step": ms_m,
                           "launches_per_step": m},
-        "ratio": ms_h / ms_m}))
+        "homogeneous_per_map_weighted": {"value": n / (ms_mix * 1e-3), "ms_per_step": ms_mix,
+                                         "per_map_ms": ms_each},
+        "ratio": ms_h / ms_m, "ratio_vs_per_map": ms_mix / ms_m}))
 
 
 if __name__ == "__main__":
