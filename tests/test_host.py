@@ -107,3 +107,11 @@ def test_multimap_contracts():
         tc.multi_reset([a, a], [4, 0], seed=0)
     with pytest.raises(tc.ContractError, match="equal length"):
         tc.multi_reset([a], [4, 4], seed=0)
+
+
+def test_multimap_group_index():
+    from paper_2605_19926_b200.multimap import MultiMapBatch
+    mb = MultiMapBatch(groups=(), offsets=(0, 700, 829), n=2329, _ob=None)
+    assert [mb.group_of(i) for i in (0, 699, 700, 828, 829, 2328)] == [0, 0, 1, 1, 2, 2]
+    with pytest.raises(tc.ContractError):
+        mb.group_of(2329)
