@@ -1178,6 +1178,9 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         const int r0 = vtop > 0 ? vtop : 0, r1 = vbot < H ? vbot : H;
         if (vbot - vtop <= 0 || r0 >= r1) continue;
         bool any = false;
+#if TC_SETUP_ROLLED
+#pragma unroll 1
+#endif
         for (int c = lane; c < W; c += G) {
           if (!(sm.zbuf(S)[c] <= d)) {
             const double a = (S.coef[c] - ks) / halfk;
@@ -1630,7 +1633,10 @@ __device__ __noinline__ void draw_sprites_direct(const SpecDev& S, WarpSmem sm, 
     const bool key = r.kd == K_KEY;
     // column terms of the lane's own columns -> shared memory; visible span
     int lo = 0x7fffffff, hi = -1;
-#pragma unroll
+    // kept rolled: one copy of the column terms (fp64 divide + mask
+    // branches) instead of NC keeps the sprite path's code footprint small
+    // (instruction-fetch bound on sprite-heavy maps; -3..-10 % step time there)
+#pragma unroll 1
     for (int j = 0; j < NC; j++) {
       const int c = lane + G * j;
       if (c >= W) continue;
