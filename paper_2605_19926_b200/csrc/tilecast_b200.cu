@@ -1178,9 +1178,8 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         const int r0 = vtop > 0 ? vtop : 0, r1 = vbot < H ? vbot : H;
         if (vbot - vtop <= 0 || r0 >= r1) continue;
         bool any = false;
-#if TC_SETUP_ROLLED
+        // rolled for code footprint, like draw_sprites_direct's column terms
 #pragma unroll 1
-#endif
         for (int c = lane; c < W; c += G) {
           if (!(sm.zbuf(S)[c] <= d)) {
             const double a = (S.coef[c] - ks) / halfk;
