@@ -274,9 +274,9 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
         N.check(rc, "tc_batch_step_mapped")
     if stg.h_flag[0]:
         # the kernel saw an action outside the contract: the step is void
-        # (bs is still valid); clear the sticky status and raise the
-        # reference's error for the first offending action
-        bs._counters.zero_()
+        # (bs is still valid; on this path the kernel reports bad actions
+        # through the flag only, so the sticky fault counters are untouched)
+        # -- raise the reference's error for the first offending action
         _check_host_actions(bs, acts)
         raise ContractError("action outside the spec's action set")
     rewards = stg.h_rew.copy()

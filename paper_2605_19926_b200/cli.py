@@ -49,7 +49,11 @@ def bench(env_id: str, n: int, steps: int, seed: int, width: int, height: int) -
     # untimed rollout for the reward accounting (cli.py:76-81)
     bs = batch_reset(spec, n, seed)
     res = rollout(bs, steps, seed, record=True)
-    reward_sum = float(res["rewards"].sum().item())
+    # summed step by step in the reference's order (cli.py:76-81): one numpy
+    # sum per step, accumulated in a Python float
+    reward_sum = 0.0
+    for row in res["rewards"].cpu().numpy():
+        reward_sum += float(row.sum())
     # device-resident fused rollout rate, for reference
     rb = batch_reset(spec, n, seed)
     torch.cuda.synchronize()

@@ -1408,7 +1408,11 @@ __device__ __forceinline__ int render_walls(const SpecDev& S, const uint32_t* __
   // fast march when the rim is sealed, the origin is on the grid and the
   // stop codes sit in shared memory; every other case runs out of line so
   // the hot kernel body stays compact (instruction-cache footprint)
-  const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h;
+  // (a zero view direction -- only reachable through a restored state or
+  // tc_host_render_into -- makes every ray (0, 0): the checked march then
+  // reports the step budget like the reference instead of spinning)
+  const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h &&
+                      (e.dx != 0.0 || e.dy != 0.0);
   const int st = (S.sealed && inside && S.smem_map && S.n_doors < 32 && S.w >= 2)
       ? wall_pass<NC, false, G, true>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
       : wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo,
@@ -2078,36 +2082,42 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   // host path). Several waves: env grp*grid + cta first, then envs pulled
   // from a self-resetting device ticket counter (the last CTA to finish
   // zeroes it for the next launch).
+  // Without counters (no ticket word) a multi-wave batch is interleaved
+  // statically: env grp*grid + cta, then + stride.
   const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
-  const bool dyn = counters != nullptr && n > stride;
-  const int epc = dyn ? 0 : (int)((n + gridDim.x - 1) / gridDim.x);
+  const bool one_wave = n <= stride;
+  const bool dyn = !one_wave && counters != nullptr;
+  const int epc = one_wave ? (int)((n + gridDim.x - 1) / gridDim.x) : 0;
   const long long cbase = (long long)blockIdx.x * epc;
-  const int cta_envs = dyn ? 0 : (int)max(0LL, min((long long)epc, n - cbase));
+  const int cta_envs = one_wave ? (int)max(0LL, min((long long)epc, n - cbase)) : 0;
   // no env for this CTA; it still counts itself done on the mapped host path
-  if ((dyn ? (long long)blockIdx.x >= n : cta_envs == 0) && !out.res_host) return;
-  const long long i_first = dyn ? (long long)grp * gridDim.x + blockIdx.x
-                                : (grp < cta_envs ? cbase + grp : n);
+  if ((one_wave ? cta_envs == 0 : (long long)blockIdx.x >= n) && !out.res_host) return;
+  const long long i_first = one_wave ? (grp < cta_envs ? cbase + grp : n)
+                                     : (long long)grp * gridDim.x + blockIdx.x;
   // per-CTA scratch after the group windows: actions / rewards / dones of
   // the CTA's envs (one-wave mapping)
   uint8_t* cta_s = smem + map_bytes + WARPS_PER_CTA * NG * S.warp_smem;
   long long* act_s = reinterpret_cast<long long*>(cta_s);
   double* rew_s = reinterpret_cast<double*>(cta_s + 64);
   uint8_t* done_s = cta_s + 128;
-  // the actions are loaded before the map staging and the dependent-launch
-  // wait so their latency (HBM, or the host bus on the mapped host path)
-  // overlaps them; actions are inputs, never written by the preceding step
-  // kernel
+  // On the mapped host path (tc_batch_step_mapped) the host wrote the
+  // actions to pinned memory before the launch, so they are fetched before
+  // the map staging and the dependent-launch wait (their bus latency overlaps
+  // both). Device-resident actions may come from the kernel just before this
+  // one on the stream (a policy draw, a policy network): they are read only
+  // after griddepcontrol.wait, which makes that kernel's writes visible.
   const bool warp0 = threadIdx.x < 32;
+  const bool early = out.res_host != nullptr;
   long long a_pre = 0;
-  if (mode == MODE_STEP) {
-    if (!dyn) {
+  if (mode == MODE_STEP && early) {
+    if (one_wave) {
       if (warp0 && (int)threadIdx.x < cta_envs) a_pre = actions[cbase + threadIdx.x];
     } else if (i_first < n) {
       a_pre = actions[i_first];
     }
   }
   stage_map_issue(S, smap, cell, solid);
-  if (!dyn && warp0 && (int)threadIdx.x < cta_envs) {
+  if (one_wave && warp0 && (int)threadIdx.x < cta_envs) {
     act_s[threadIdx.x] = a_pre;
     rew_s[threadIdx.x] = 0.0;
     done_s[threadIdx.x] = 0;
@@ -2136,7 +2146,8 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     } else {
       load_env<G>(S, st, i, e);
       if (mode == MODE_STEP) {
-        const long long act = i != i_first ? actions[i] : (dyn ? a_pre : act_s[grp]);
+        const long long act = (early && i == i_first) ? (one_wave ? act_s[grp] : a_pre)
+                                                      : actions[i];
         TRACE(i, 1);
         if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
           status = TC_ST_BAD_ACTION;
@@ -2149,7 +2160,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
             out.dones[i] = (uint8_t)o.done;
             out.truncs[i] = (uint8_t)o.trunc;
             out.events[i] = o.events;
-            if (!dyn && out.res_host) {
+            if (one_wave && out.res_host) {
               rew_s[grp] = o.reward;
               done_s[grp] = (uint8_t)o.done;
             }
@@ -2169,7 +2180,10 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
                                  lg, i);
     }
     if (lane == 0) out.statuses[i] = status;
-    if (status != TC_ST_OK) badbits |= 1u << status;
+    // a bad action on the mapped host path is reported through flag_host
+    // only (the host voids the step); the sticky counters keep real faults
+    if (status != TC_ST_OK && !(status == TC_ST_BAD_ACTION && out.flag_host))
+      badbits |= 1u << status;
 #if TC_TRACE
     if (g_trace && lane == 0) {
       unsigned int smid;
@@ -2192,7 +2206,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     // every warp is done with its shared memory: word 0 carries the flag
     volatile int& s_last = *reinterpret_cast<int*>(smem);
     __syncthreads();
-    if (!dyn && out.res_host) {
+    if (one_wave && out.res_host) {
       // one-wave mapping: the CTA's contiguous rewards / dones go to pinned
       // host memory as one run each, made visible system-wide before the CTA
       // counts itself done (a voided bad-action env keeps reward 0, done 0)
@@ -2214,7 +2228,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       s_last = last;
     }
     __syncthreads();
-    if (s_last && out.res_host && !dyn) {
+    if (s_last && out.res_host && one_wave) {
       // every CTA's results reached host memory before it was counted
       if (threadIdx.x == 0) {
         __threadfence_system();
