@@ -127,8 +127,36 @@ struct SpecDev {
   int o_t0, o_b0, o_t8, o_wrgb, o_zbuf, o_gdep, o_recs, o_band;  // WarpSmem offsets
   int o_wpk, o_tpk;  // contig compose: packed wall RGB / per-byte top row streams
   int o_sct;         // contig sprites: per-column terms (f64[W] then u8[W] flags)
+  int o_srow;        // contig sprites: per-row terms (f64[H] then u8[H] flags)
   int warp_smem;     // bytes of per-warp shared memory
+  // Read-only tables staged per CTA into shared memory (smem offset = blob
+  // offset): [coef | pal | doorrgb | epx | epy | spx | spy | goal_ent | dcol |
+  // dlock | ekind | ecol] always, then [cells | guarded stop codes] when the
+  // map fits (smem_map). stage_bytes = the staged prefix of the blob.
+  const uint8_t* blob;
+  int b_coef, b_pal, b_door, b_epx, b_epy, b_spx, b_spy, b_goal, b_dcol, b_dlock, b_ekind,
+      b_ecol, b_cell, b_solid;
+  int stage_bytes;
 };
+
+// the dynamic shared memory of every kernel that stages a spec
+extern __shared__ __align__(16) uint8_t g_smem[];
+template <class T>
+__device__ __forceinline__ const T* stab(int off) {
+  return reinterpret_cast<const T*>(g_smem + off);
+}
+#define T_COEF(S) stab<double>((S).b_coef)
+#define T_PAL(S) stab<uint32_t>((S).b_pal)
+#define T_DOOR(S) stab<uint32_t>((S).b_door)
+#define T_EPX(S) stab<double>((S).b_epx)
+#define T_EPY(S) stab<double>((S).b_epy)
+#define T_SPX(S) stab<double>((S).b_spx)
+#define T_SPY(S) stab<double>((S).b_spy)
+#define T_GOAL(S) stab<int32_t>((S).b_goal)
+#define T_DCOL(S) stab<uint8_t>((S).b_dcol)
+#define T_DLOCK(S) stab<uint8_t>((S).b_dlock)
+#define T_EKIND(S) stab<uint8_t>((S).b_ekind)
+#define T_ECOL(S) stab<uint8_t>((S).b_ecol)
 
 struct StateDev {
   double *px, *py, *dx, *dy, *health;
@@ -187,6 +215,12 @@ struct SpriteRec {
 
 #if TC_TRACE
 __device__ unsigned long long* g_trace = nullptr;
+// per-CTA launch timeline [generation][cta][4]: entry, map staged, past
+// griddepcontrol.wait, exit; the generation of a CTA is the number of
+// earlier launches whose CTA of the same index entered (PDL starts every
+// CTA of a launch before any CTA of its dependent)
+__device__ unsigned long long* g_trace_cta = nullptr;
+__device__ unsigned int g_cta_gen[16384];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -370,8 +404,8 @@ __device__ __forceinline__ uint64_t scan_tiles(const SpecDev& S, const uint32_t*
           uint32_t dm = dmask;
           if (code != 0xffffffffu && (code & ~dm) != 0u && touch) {  // closed door
             const int di = (int)(cell[ty * S.w + tx] & 31u);
-            const int dc = S.dcol[di];
-            if (!(S.dlock[di] != 0 && ((inv >> dc) & 1u) == 0)) {
+            const int dc = T_DCOL(S)[di];
+            if (!(T_DLOCK(S)[di] != 0 && ((inv >> dc) & 1u) == 0)) {
               opened = 1u << di;
               events = 1u << (EV_DOOR_BASE_BIT + dc);
               dm |= opened;
@@ -393,16 +427,16 @@ __device__ __forceinline__ uint64_t scan_tiles(const SpecDev& S, const uint32_t*
 __device__ __forceinline__ void reset_draws_inl(const SpecDev& S, Env& e) {
   unsigned long long ctr = e.rctr;
   uint64_t v = draw_below(e.rkey, ctr, (uint64_t)S.n_spawns);
-  e.x = S.spx[v];
-  e.y = S.spy[v];
+  e.x = T_SPX(S)[v];
+  e.y = T_SPY(S)[v];
   v = draw_below(e.rkey, ctr, 4);
   e.dx = S.dirs[2 * v];
   e.dy = S.dirs[2 * v + 1];
   if (S.goal_mode == 1 && S.n_goals > 0) {
     v = draw_below(e.rkey, ctr, (uint64_t)S.n_goals);
-    e.agoal = S.goal_ent[v];
+    e.agoal = T_GOAL(S)[v];
   } else if (S.n_goals > 0) {
-    e.agoal = S.goal_ent[0];
+    e.agoal = T_GOAL(S)[0];
   } else {
     e.agoal = -1;
   }
@@ -480,9 +514,9 @@ __device__ __forceinline__ StepOut step_dynamics(const SpecDev& S, const uint32_
   const int ctx = (int)floor(x), cty = (int)floor(y);
   const int ent = (int)((cell[cty * S.w + ctx] >> CELL_EAT_SHIFT) & 0xffu) - 1;
   if (ent >= 0 && ((e.emask >> ent) & 1ULL)) {
-    const int kd = S.ekind[ent];
+    const int kd = T_EKIND(S)[ent];
     if (kd == K_KEY) {
-      const int col = S.ecol[ent];
+      const int col = T_ECOL(S)[ent];
       e.inv = (e.inv | (1u << col)) & 0xffu;
       e.emask &= ~(1ULL << ent);
       o.events |= 1u << (EV_KEY_BASE_BIT + col);
@@ -576,6 +610,10 @@ struct WarpSmem {
   __device__ __forceinline__ uint8_t* scf(const SpecDev& S) const {
     return base + S.o_sct + 8 * ((S.obs_w + 15) & ~15);
   }
+  __device__ __forceinline__ double* srt(const SpecDev& S) const { return (double*)(base + S.o_srow); }
+  __device__ __forceinline__ uint8_t* srf(const SpecDev& S) const {
+    return base + S.o_srow + 8 * ((S.obs_h + 15) & ~15);
+  }
   __device__ __forceinline__ double* zbuf(const SpecDev& S) const { return (double*)(base + S.o_zbuf); }
   __device__ __forceinline__ double* gdep(const SpecDev& S) const { return (double*)(base + S.o_gdep); }
   __device__ __forceinline__ SpriteRec* recs(const SpecDev& S) const { return (SpriteRec*)(base + S.o_recs); }
@@ -610,6 +648,7 @@ __host__ inline int warp_smem_layout(SpecDev& d, int nbands) {
   d.o_wpk = off; off += d.contig ? align16(3 * wp) : 0;
   d.o_tpk = off; off += d.contig ? align16(3 * wp) : 0;
   d.o_sct = off; off += d.contig ? align16(9 * wp) : 0;
+  d.o_srow = off; off += d.contig ? align16(9 * ((d.obs_h + 15) & ~15)) : 0;
   return align16(off);
 }
 
@@ -994,26 +1033,15 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
   const int ox = (int)floor(e.x), oy = (int)floor(e.y);
   const double atten = S.fc[FC_ATTEN];
   int bad_col = 0x7fffffff, bad_status = TC_ST_OK;
-  // per-column result -> zbuf / spans / shaded colour, _pycore.py:159-178
-  auto column_out = [&](int c, const March& r) {
-    if (rayinfo) {
-      int mx, my;
-      if (CHECKED && r.status != TC_ST_OK) { mx = (int)r.sdx; my = (int)r.sdy; }
-      else { my = r.idx / mw; mx = r.idx - my * mw; }
-      rayinfo[c * 4 + 0] = mx; rayinfo[c * 4 + 1] = my;
-      rayinfo[c * 4 + 2] = r.xs ? 0 : 1; rayinfo[c * 4 + 3] = r.steps;
-    }
-    if (CHECKED && r.status != TC_ST_OK) {
-      if (c < bad_col) { bad_col = c; bad_status = r.status; }
-      return;
-    }
-    const double perp = r.xs ? r.sdx - r.ddx : r.sdy - r.ddy;
+  // the shaded wall slice of column c from its perpendicular distance and
+  // hit cell (the ray state itself is dead by now)
+  auto col_write = [&](int c, double perp, int hit) {
     sm.zbuf(S)[c] = perp;
     if (zbuf_out) zbuf_out[c] = perp;
     const double shade = 1.0 / (1.0 + atten * perp);
-    const uint32_t cw = cell[r.idx];
-    const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? S.doorrgb[cw & 31u]
-                                                                     : S.pal[cw & 0xffu];
+    const uint32_t cw = cell[hit];
+    const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? T_DOOR(S)[cw & 31u]
+                                                                     : T_PAL(S)[cw & 0xffu];
     const uint32_t rgb = rgb_scale(base, shade);
     double lh_f = (double)H / perp;
     if (lh_f > 1e9) lh_f = 1e9;
@@ -1033,6 +1061,21 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
       sm.b0(S)[c] = (uint16_t)(bot < H ? bot : H);
     }
   };
+  // per-column result -> zbuf / spans / shaded colour, _pycore.py:159-178
+  auto column_out = [&](int c, const March& r) {
+    if (rayinfo) {
+      int mx, my;
+      if (CHECKED && r.status != TC_ST_OK) { mx = (int)r.sdx; my = (int)r.sdy; }
+      else { my = r.idx / mw; mx = r.idx - my * mw; }
+      rayinfo[c * 4 + 0] = mx; rayinfo[c * 4 + 1] = my;
+      rayinfo[c * 4 + 2] = r.xs ? 0 : 1; rayinfo[c * 4 + 3] = r.steps;
+    }
+    if (CHECKED && r.status != TC_ST_OK) {
+      if (c < bad_col) { bad_col = c; bad_status = r.status; }
+      return;
+    }
+    col_write(c, r.xs ? r.sdx - r.ddx : r.sdy - r.ddy, r.idx);
+  };
   int c = lane;
   if (FAST || (!CHECKED && S.smem_map && S.n_doors < 32 && mw >= 2)) {
     // shared-memory stop codes, predicated lockstep march (march_fast):
@@ -1045,7 +1088,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
       FastRay fr[LR];
 #pragma unroll
       for (int q = 0; q < LR; q++) {
-        const double k = S.coef[c + q * G];
+        const double k = T_COEF(S)[c + q * G];
         const RaySetup rs = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k, e.dy + planey * k);
         fr[q].sdx = rs.sdx; fr[q].sdy = rs.sdy; fr[q].ddx = rs.ddx; fr[q].ddy = rs.ddy;
         fr[q].addr = sbase + 4u * (uint32_t)idx0;
@@ -1053,19 +1096,31 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
         fr[q].last = fr[q].incx;
       }
       march_fast<LR>(smask, fr);
+      if (rayinfo) {
 #pragma unroll
-      for (int q = 0; q < LR; q++) {
-        March r;
-        r.sdx = fr[q].sdx; r.sdy = fr[q].sdy; r.ddx = fr[q].ddx; r.ddy = fr[q].ddy;
-        r.idx = (int)(fr[q].addr - sbase) >> 2;
-        r.xs = fr[q].last == fr[q].incx;
-        r.status = TC_ST_OK;
-        r.steps = 0;
-        if (rayinfo) {
+        for (int q = 0; q < LR; q++) {
+          March r;
+          r.sdx = fr[q].sdx; r.sdy = fr[q].sdy; r.ddx = fr[q].ddx; r.ddy = fr[q].ddy;
+          r.idx = (int)(fr[q].addr - sbase) >> 2;
+          r.xs = fr[q].last == fr[q].incx;
+          r.status = TC_ST_OK;
           const int my = r.idx / mw, mx = r.idx - my * mw;
           r.steps = abs(mx - ox) + abs(my - oy);
+          column_out(c + q * G, r);
         }
-        column_out(c + q * G, r);
+      } else {
+        // reduce every ray to (perp, hit cell) first: the sdx/sdy/ddx/ddy
+        // of the later rays are not kept live across the earlier ones' writes
+        double perp[LR];
+        int hit[LR];
+#pragma unroll
+        for (int q = 0; q < LR; q++) {
+          const bool xs = fr[q].last == fr[q].incx;
+          perp[q] = xs ? fr[q].sdx - fr[q].ddx : fr[q].sdy - fr[q].ddy;
+          hit[q] = (int)(fr[q].addr - sbase) >> 2;
+        }
+#pragma unroll
+        for (int q = 0; q < LR; q++) col_write(c + q * G, perp[q], hit[q]);
       }
     };
     constexpr int LR = TC_LOCKSTEP;
@@ -1084,7 +1139,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
       March rr[LR];
 #pragma unroll
       for (int q = 0; q < LR; q++) {
-        const double k = S.coef[c + q * G];
+        const double k = T_COEF(S)[c + q * G];
         rs[q] = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k, e.dy + planey * k);
       }
       march_n<LR>(solid, e.dmask, rs, rr);
@@ -1093,7 +1148,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     }
 #pragma unroll 1
     for (; c + G < W; c += 2 * G) {
-      const double k0 = S.coef[c], k1 = S.coef[c + G];
+      const double k0 = T_COEF(S)[c], k1 = T_COEF(S)[c + G];
       RaySetup a = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k0, e.dy + planey * k0);
       RaySetup b = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k1, e.dy + planey * k1);
       March ra, rb;
@@ -1104,7 +1159,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
   }
 #pragma unroll 1
   for (; c < W; c += G) {
-    const double k = S.coef[c];
+    const double k = T_COEF(S)[c];
     const double rx = e.dx + planex * k;
     const double ry = e.dy + planey * k;
     const March r = march<CHECKED>(solid, mw, S.h, e.dmask, e.x, e.y, ox, oy, rx, ry);
@@ -1122,8 +1177,9 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
 
 // Sprite gather (entity order, _pycore.py:192-209) and per-sprite
 // parameters (:219-252). Sprites that provably draw nothing -- denom <= 0,
-// an empty row span, or no column with zbuf[c] > dep and |a| < 1 (the
-// reference's own per-column tests, evaluated exactly) -- are dropped
+// an empty row span, or (debug-tap builds only; the draw repeats the test)
+// no column with zbuf[c] > dep and |a| < 1 (the reference's own per-column
+// tests, evaluated exactly) -- are dropped
 // here; the survivors keep their relative order, so the stable far->near
 // sort (= the reference's insertion sort, :210-217) of the survivors is the
 // reference's order restricted to sprites that draw. Returns the survivor
@@ -1146,9 +1202,9 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
       bool keep = false;
       double lat = 0.0, dep = 0.0;
       if (ent < S.n_ent && ((e.emask >> ent) & 1ULL) &&
-          !(S.ekind[ent] == K_GOAL && ent != e.agoal)) {
-        const double relx = S.epx[ent] - e.x;
-        const double rely = S.epy[ent] - e.y;
+          !(T_EKIND(S)[ent] == K_GOAL && ent != e.agoal)) {
+        const double relx = T_EPX(S)[ent] - e.x;
+        const double rely = T_EPY(S)[ent] - e.y;
         lat = invdet * (e.dy * relx - e.dx * rely);
         dep = invdet * (-planey * relx + planex * rely);
         keep = !(dep < S.fc[FC_MIN_SPRITE_DEPTH]);
@@ -1177,16 +1233,20 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
         const int vtop = h2 - vhalf, vbot = h2 + vhalf;
         const int r0 = vtop > 0 ? vtop : 0, r1 = vbot < H ? vbot : H;
         if (vbot - vtop <= 0 || r0 >= r1) continue;
-        bool any = false;
-        // rolled for code footprint, like draw_sprites_direct's column terms
+        if (spritevis_out) {
+          // debug tap: keep exactly the sprites with a visible column (the
+          // draw evaluates the same per-column test; a sprite with none
+          // draws nothing, so the frames do not depend on this filter)
+          bool any = false;
 #pragma unroll 1
-        for (int c = lane; c < W; c += G) {
-          if (!(sm.zbuf(S)[c] <= d)) {
-            const double a = (S.coef[c] - ks) / halfk;
-            any |= !(a <= -1.0 || a >= 1.0);
+          for (int c = lane; c < W; c += G) {
+            if (!(sm.zbuf(S)[c] <= d)) {
+              const double a = (T_COEF(S)[c] - ks) / halfk;
+              any |= !(a <= -1.0 || a >= 1.0);
+            }
           }
+          if (!g.any(any)) continue;
         }
-        if (!g.any(any)) continue;
         const int en = base + src;
         if (lane == 0) {
           SpriteRec r;
@@ -1197,9 +1257,9 @@ __device__ __forceinline__ int sprite_setup(const SpecDev& S, const WarpSmem& sm
           r.denom = vbot - vtop;
           r.r0 = r0;
           r.r1 = r1;
-          r.kd = S.ekind[en];
+          r.kd = T_EKIND(S)[en];
           r.ent = en;
-          const uint32_t m1 = r.kd == K_KEY ? S.key_rgb[S.ecol[en]]
+          const uint32_t m1 = r.kd == K_KEY ? S.key_rgb[T_ECOL(S)[en]]
                               : r.kd == K_GOAL ? S.goal_rgb : S.med_cross;
           r.s1 = rgb_scale(m1, shade);
           r.s2 = rgb_scale(S.med_box, shade);
@@ -1284,7 +1344,7 @@ __device__ __forceinline__ void draw_sprites(const SpecDev& S, const WarpSmem& s
         ct[j] = 0.0;
         cf[j] = 0;
         if (c < W && !(sm.zbuf(S)[c] <= r.dep)) {
-          const double a = (S.coef[c] - r.ks) / r.halfk;
+          const double a = (T_COEF(S)[c] - r.ks) / r.halfk;
           if (!(a <= -1.0 || a >= 1.0)) {
             vis[j] = true;
             const double aa = a >= 0.0 ? a : -a;
@@ -1617,11 +1677,55 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
   g.sync();
 }
 
-// Sprites over a directly stored frame (contig compose): same terms and
-// comparisons as draw_sprites, but the lanes are remapped onto the sprite's
-// visible column span [lo, hi] (per-column terms go through shared memory),
-// so a sprite w columns wide costs ceil(w / G) column slots per row instead
-// of W / G. Pixels leave as one 16-bit + one 8-bit store.
+// Pixels of one sprite over its visible rectangle [lo, lo + w) x [r0, r0 + h):
+// the rectangle is walked row-major with the lanes strided over it (every
+// lane busy whatever the sprite's shape), each pixel's mask evaluated from
+// the per-column and per-row terms in shared memory (_pycore.py:99-129
+// split into exact column and row factors: the same doubles and comparisons
+// as the reference), and the pixel written as one 16-bit + one 8-bit store.
+template <int KIND, int G>
+__device__ __forceinline__ void sprite_pixels(uint8_t* __restrict__ frame, int row_bytes, int lo,
+                                              int w, int r0, int h, const double* sct,
+                                              const uint8_t* scf, const double* srt,
+                                              const uint8_t* srf, uint32_t s1, uint32_t s2,
+                                              int lane) {
+  const int npx = w * h;
+  int pr = lane / w, pc = lane - (lane / w) * w;
+  const int dr = G / w, dc = G - (G / w) * w;
+#pragma unroll 1
+  for (int p = lane; p < npx; p += G) {
+    const int c = lo + pc, r = r0 + pr;
+    const int cf = scf[c];
+    if (cf & 0x80) {
+      int mk;
+      if (KIND == K_GOAL) {
+        mk = (sct[c] + srt[r] <= 0.8) ? 1 : 0;  // aa + |v-0.5|*2.0 <= 0.8
+      } else if (KIND == K_KEY) {
+        const double e = sct[c] + srt[r];      // ea*ea + ev*ev
+        mk = ((0.30 <= e && e <= 1.0) || (cf & srf[r] & 7) != 0) ? 1 : 0;
+      } else {
+        const int x = cf & srf[r] & 7;
+        mk = (x & 3) ? 1 : ((x & 4) ? 2 : 0);
+      }
+      if (mk) {
+        const uint32_t col = mk == 1 ? s1 : s2;
+        uint8_t* d = frame + (size_t)r * row_bytes + c * 3;
+        const int odd = (int)(reinterpret_cast<uintptr_t>(d) & 1u);
+        *reinterpret_cast<uint16_t*>(d + odd) = (uint16_t)(col >> (8 * odd));
+        d[odd ? 0 : 2] = (uint8_t)(odd ? col : col >> 16);
+      }
+    }
+    pc += dc;
+    pr += dr;
+    if (pc >= w) { pc -= w; pr++; }
+  }
+}
+
+// Sprites over a directly stored frame (contig compose), in draw order:
+// per sprite, the lanes compute the column terms of their own columns
+// (shared memory; visible span [lo, hi] by group min / max) and the row
+// terms of rows [r0, r1) (shared memory, one division per row), then
+// sprite_pixels walks the visible rectangle.
 template <int NC, int G>
 __device__ __noinline__ void draw_sprites_direct(const SpecDev& S, WarpSmem sm, int m,
                                                  uint8_t* __restrict__ frame) {
@@ -1630,24 +1734,20 @@ __device__ __noinline__ void draw_sprites_direct(const SpecDev& S, WarpSmem sm, 
   const int W = S.obs_w, row_bytes = W * 3;
   double* sct = sm.sct(S);
   uint8_t* scf = sm.scf(S);
+  double* srt = sm.srt(S);
+  uint8_t* srf = sm.srf(S);
+#pragma unroll 1
   for (int s = 0; s < m; s++) {
     const SpriteRec r = sm.recs(S)[s];
-    const double denom = (double)r.denom;
     const bool key = r.kd == K_KEY;
-    // column terms of the lane's own columns -> shared memory; visible span
     int lo = 0x7fffffff, hi = -1;
-    // kept rolled: one copy of the column terms (fp64 divide + mask
-    // branches) instead of NC keeps the sprite path's code footprint small
-    // (instruction-fetch bound on sprite-heavy maps; -3..-10 % step time there)
 #pragma unroll 1
-    for (int j = 0; j < NC; j++) {
-      const int c = lane + G * j;
-      if (c >= W) continue;
+    for (int c = lane; c < W; c += G) {
       double ct = 0.0;
       int cf = 0;
       bool vis = false;
       if (!(sm.zbuf(S)[c] <= r.dep)) {
-        const double a = (S.coef[c] - r.ks) / r.halfk;
+        const double a = (T_COEF(S)[c] - r.ks) / r.halfk;
         if (!(a <= -1.0 || a >= 1.0)) {
           vis = true;
           const double aa = a >= 0.0 ? a : -a;
@@ -1669,68 +1769,38 @@ __device__ __noinline__ void draw_sprites_direct(const SpecDev& S, WarpSmem sm, 
     lo = g.min(lo);
     hi = g.max(hi);
     if (hi < 0) continue;
+    const double denom = (double)r.denom;
+#pragma unroll 1
+    for (int row = r.r0 + lane; row < r.r1; row += G) {
+      const double v = ((double)(row - r.vtop) + 0.5) / denom;
+      double rt = 0.0;
+      int rf = 0;
+      if (r.kd == K_GOAL) {
+        double dv = v - 0.5;
+        if (dv < 0.0) dv = -dv;
+        rt = dv * 2.0;
+      } else if (key) {
+        const double ev = (v - 0.30) / 0.18;
+        rt = ev * ev;
+        rf = (0.30 <= v && v <= 0.85 ? 1 : 0) | (0.62 <= v && v <= 0.70 ? 2 : 0) |
+             (0.76 <= v && v <= 0.84 ? 4 : 0);
+      } else {
+        rf = (0.32 <= v && v <= 0.73 ? 1 : 0) | (0.47 <= v && v <= 0.60 ? 2 : 0) |
+             (0.25 <= v && v <= 0.80 ? 4 : 0);
+      }
+      srt[row] = rt;
+      srf[row] = (uint8_t)rf;
+    }
     g.sync();
-    const int ncv = (hi - lo + G) / G;  // column slots over [lo, hi]
-    double ct[NC];
-    int cf[NC];
-#pragma unroll
-    for (int j = 0; j < NC; j++) {
-      const int c = lo + lane + G * j;
-      const bool in = j < ncv && c <= hi;
-      ct[j] = in ? sct[c] : 0.0;
-      cf[j] = in ? scf[c] : 0;
-    }
-    const int ra = r.r0, rb = r.r1;
-    for (int r32 = ra; r32 < rb; r32 += G) {
-      // lane-parallel row terms (_pycore.py:99-129 split into factors)
-      double rt_l = 0.0;
-      int rf_l = 0;
-      if (r32 + lane < rb) {
-        const double v = ((double)(r32 + lane - r.vtop) + 0.5) / denom;
-        if (r.kd == K_GOAL) {
-          double dv = v - 0.5;
-          if (dv < 0.0) dv = -dv;
-          rt_l = dv * 2.0;
-        } else if (key) {
-          const double ev = (v - 0.30) / 0.18;
-          rt_l = ev * ev;
-          rf_l = (0.30 <= v && v <= 0.85 ? 1 : 0) | (0.62 <= v && v <= 0.70 ? 2 : 0) |
-                 (0.76 <= v && v <= 0.84 ? 4 : 0);
-        } else {
-          rf_l = (0.32 <= v && v <= 0.73 ? 1 : 0) | (0.47 <= v && v <= 0.60 ? 2 : 0) |
-                 (0.25 <= v && v <= 0.80 ? 4 : 0);
-        }
-      }
-      const int nr = min(G, rb - r32);
-      for (int k = 0; k < nr; k++) {
-        const double rt = g.shfl(rt_l, k);
-        const int rf = g.shfl(rf_l, k);
-        uint8_t* drow = frame + (size_t)(r32 + k) * row_bytes;
-#pragma unroll
-        for (int j = 0; j < NC; j++) {
-          if (j >= ncv) break;
-          if (!(cf[j] & 0x80)) continue;
-          int mk;
-          if (r.kd == K_GOAL) {
-            mk = (ct[j] + rt <= 0.8) ? 1 : 0;  // aa + |v-0.5|*2.0 <= 0.8
-          } else if (key) {
-            const double e = ct[j] + rt;        // ea*ea + ev*ev
-            mk = ((0.30 <= e && e <= 1.0) || (cf[j] & rf & 7) != 0) ? 1 : 0;
-          } else {
-            const int x = cf[j] & rf & 7;
-            mk = (x & 3) ? 1 : ((x & 4) ? 2 : 0);
-          }
-          if (mk) {
-            const uint32_t col = mk == 1 ? r.s1 : r.s2;
-            uint8_t* d = drow + (lo + lane + G * j) * 3;
-            const int odd = (int)(reinterpret_cast<uintptr_t>(d) & 1u);
-            *reinterpret_cast<uint16_t*>(d + odd) = (uint16_t)(col >> (8 * odd));
-            d[odd ? 0 : 2] = (uint8_t)(odd ? col : col >> 16);
-          }
-        }
-      }
-    }
-    g.sync();  // the next sprite reuses the column-term scratch
+    const int w = hi - lo + 1, h = r.r1 - r.r0;
+    if (r.kd == K_GOAL)
+      sprite_pixels<K_GOAL, G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2, lane);
+    else if (key)
+      sprite_pixels<K_KEY, G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2, lane);
+    else
+      sprite_pixels<K_MEDKIT, G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2,
+                                 lane);
+    g.sync();  // the next sprite reuses the term scratch; pixel order = draw order
   }
 }
 
@@ -1954,6 +2024,18 @@ __device__ __forceinline__ int render_env(const SpecDev& S, const uint32_t* __re
   TRACE(ti, 3);
   const int m = render_sprites<G>(S, sm, e, spritevis_out);
   TRACE(ti, 4);
+#if TC_TRACE
+  if (g_trace && Grp<G>().lane == 0) {
+    // sprites drawn and their pixel footprint (rows x visible-column bound)
+    unsigned long long px = 0;
+    for (int k = 0; k < m; k++) {
+      const SpriteRec r = sm.recs(S)[k];
+      const double w = 2.0 * r.halfk * (S.obs_w - 1) / 2.0;
+      px += (unsigned long long)(r.r1 - r.r0) * (unsigned long long)(w < S.obs_w ? w : S.obs_w);
+    }
+    g_trace[ti * 8 + 7] = (unsigned long long)m | (px << 8);
+  }
+#endif
   render_frame_out<NC, G>(S, sm, m, frame, bulk_pending, buf, lg);
   return TC_ST_OK;
 }
@@ -2008,36 +2090,29 @@ __device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, 
     st.ealive[i * S.n_ent + k] = (uint8_t)((e.emask >> k) & 1ULL);
 }
 
-// packed cells + stop codes into shared memory once per CTA: [cells,
-// padded to 4 words | stop codes with their wall guards, padded to 4 words],
-// copied as 16-byte cp.async chunks (all in flight at once; the blob's
-// entries are 16-byte aligned and padded, so the rounded-up tail reads stay
-// inside it)
-__host__ __device__ __forceinline__ int map_words_cells(int h, int w) { return (h * w + 3) & ~3; }
-__host__ __device__ __forceinline__ int map_words_solid(int h, int w) {
-  return (h * w + 2 * (w + 1) + 3) & ~3;
-}
-__host__ __device__ __forceinline__ int map_smem_bytes(const SpecDev& S) {
-  return S.smem_map ? 4 * (map_words_cells(S.h, S.w) + map_words_solid(S.h, S.w)) : 0;
-}
+// Spec staging, once per CTA: the blob prefix (the small tables -- column
+// coefficients, palette, door colours, entity / spawn / goal arrays -- and,
+// when the map fits, the packed cells and guarded stop codes) is copied to
+// shared memory at the same offsets, so every table read on the step's
+// critical path is a shared-memory load instead of an L1/L2 round trip.
+__host__ __device__ __forceinline__ int map_smem_bytes(const SpecDev& S) { return S.stage_bytes; }
 __device__ __forceinline__ void stage_map_issue(const SpecDev& S, uint32_t* smap,
                                                 const uint32_t*& cell, const uint32_t*& solid) {
-  if (!S.smem_map) {
-    cell = S.cell;
-    solid = S.solid;
-    return;
-  }
-  const int guard = S.w + 1;
-  const int wc = map_words_cells(S.h, S.w), ws = map_words_solid(S.h, S.w);
-  const int n4c = wc >> 2, n4 = (wc + ws) >> 2;
+  // the blob prefix -> shared memory at the same offsets, 16-byte cp.async
+  // chunks all in flight at once (entries are 16-byte aligned and padded)
+  const int n4 = S.stage_bytes >> 4;
   const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(smap);
   for (int k = threadIdx.x; k < n4; k += blockDim.x) {
-    const uint32_t* src = k < n4c ? S.cell + 4 * k : (S.solid - guard) + 4 * (k - n4c);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16u * k), "l"(src)
-                 : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16u * k),
+                 "l"(S.blob + 16 * k) : "memory");
   }
-  cell = smap;
-  solid = smap + wc + guard;
+  if (S.smem_map) {
+    cell = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(smap) + S.b_cell);
+    solid = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(smap) + S.b_solid);
+  } else {
+    cell = S.cell;
+    solid = S.solid;
+  }
 }
 __device__ __forceinline__ void stage_map_wait() {
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -2054,14 +2129,14 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
 // MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387.
 // A group of G lanes owns one env at a time (G = 32: a warp; G = 16: each
 // half of a warp runs its own env).
-template <int NC, int G, int MINB>
+template <int NC, int G, int MINB, bool TAPS>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, MINB)
 batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
              const __grid_constant__ StateDev so, const long long* __restrict__ actions,
              const __grid_constant__ OutDev out,
              long long n, int mode, int auto_reset, int validate,
              tc_counters* __restrict__ counters) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* const smem = g_smem;
   constexpr int NG = 32 / G;  // groups per warp
   const Grp<G> g;
   const int lane = g.lane;
@@ -2072,6 +2147,14 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   // programmatic dependent launch: let the next step's grid start its
   // prologue as our CTAs retire, and stage the (constant) map before
   // waiting for the previous step's state to be complete and visible
+#if TC_TRACE
+  unsigned long long tcta[4] = {0, 0, 0, 0};
+  unsigned int tgen = 0;
+  if (g_trace_cta && threadIdx.x == 0) {
+    tcta[0] = gtime();
+    tgen = atomicAdd(&g_cta_gen[blockIdx.x], 1u);
+  }
+#endif
   asm volatile("griddepcontrol.launch_dependents;");
   // no env for this CTA (n < grid); it still counts itself done when the
   // last CTA ships the results to the host
@@ -2123,7 +2206,13 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     done_s[threadIdx.x] = 0;
   }
   stage_map_wait();
+#if TC_TRACE
+  if (g_trace_cta && threadIdx.x == 0) tcta[1] = gtime();
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if TC_TRACE
+  if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
+#endif
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
   const LaneGeo lg = lane_geo<G>(S);
@@ -2173,11 +2262,13 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       }
     }
     if (status == TC_ST_OK) {
-      status = render_env<NC, G>(S, cell, solid, sm, e, out.frames + (size_t)i * frame_bytes,
-                                 out.zbuf ? out.zbuf + (size_t)i * S.obs_w : nullptr,
-                                 out.rayinfo ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
-                                 out.spritevis ? out.spritevis + i : nullptr, bulk_pending, buf,
-                                 lg, i);
+      // debug taps only in the TAPS instantiation (nullptr constants fold
+      // the tap code out of the throughput kernel)
+      status = render_env<NC, G>(
+          S, cell, solid, sm, e, out.frames + (size_t)i * frame_bytes,
+          (TAPS && out.zbuf) ? out.zbuf + (size_t)i * S.obs_w : nullptr,
+          (TAPS && out.rayinfo) ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
+          (TAPS && out.spritevis) ? out.spritevis + i : nullptr, bulk_pending, buf, lg, i);
     }
     if (lane == 0) out.statuses[i] = status;
     // a bad action on the mapped host path is reported through flag_host
@@ -2252,6 +2343,16 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
       if (threadIdx.x == 0) *(volatile int32_t*)(out.flag_host + 1) = 1;
     }
   }
+#if TC_TRACE
+  if (g_trace_cta) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tcta[3] = gtime();
+      unsigned long long* d = g_trace_cta + ((size_t)tgen * 16384 + blockIdx.x) * 4;
+      d[0] = tcta[0]; d[1] = tcta[1]; d[2] = tcta[2]; d[3] = tcta[3];
+    }
+  }
+#endif
 }
 
 // K fused steps with on-device policy actions (batch.py:141-153 draws) and
@@ -2261,7 +2362,7 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, G == 16 ? TC_MIN_CTAS16 : 
 rollout_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
                const __grid_constant__ OutDev out, long long n,
                const __grid_constant__ RolloutArgs ra, tc_counters* __restrict__ counters) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* const smem = g_smem;
   constexpr int NG = 32 / G;
   const Grp<G> g;
   const int lane = g.lane;
@@ -2350,6 +2451,8 @@ struct tc_spec {
   int max_ctas = 0;    // grid size for one full wave
   int max_ctas_w = 0;  // the same for the multi-wave (wide) step kernel
   size_t smem_bytes = 0;
+  int tab_bytes = 0;  // blob prefix holding the small tables
+  int map_bytes = 0;  // blob prefix up to the end of the guarded stop codes
 };
 
 namespace {
@@ -2390,40 +2493,46 @@ int pick_nc(int obs_w, int group) {
 // for batches that fit one wave -- the step is then a latency chain per env
 // -- and 96 registers (5 CTAs/SM, more warps to hide latency) for batches
 // that need several waves (measured: +3-6 % at 16K-131K envs, -5 % at 4K).
-template <int NC, int G, bool WIDE = false>
+// Kernel budgets: 16-lane groups in two register budgets (WIDE: 96 regs, 5
+// CTAs/SM for multi-wave batches; else 128 regs, 4 CTAs/SM, one-wave
+// batches); full-warp groups TC_MIN_CTAS (multi-wave) / TC_MIN_CTAS32_1W
+// (one-wave) CTAs per SM. TAPS = the debug-tap instantiation (zbuf / rayinfo
+// / spritevis outputs; tests only), built with the WIDE budget.
+#ifndef TC_MIN_CTAS32_1W
+#define TC_MIN_CTAS32_1W TC_MIN_CTAS
+#endif
+template <int NC, int G, bool WIDE = false, bool TAPS = false>
 const void* batch_fn() {
-  constexpr int minb = G == 16 ? (WIDE ? TC_MIN_CTAS16_WIDE : TC_MIN_CTAS16) : TC_MIN_CTAS;
-  return (const void*)batch_kernel<NC, G, minb>;
+  constexpr int minb = G == 16 ? (WIDE ? TC_MIN_CTAS16_WIDE : TC_MIN_CTAS16)
+                               : (WIDE ? TC_MIN_CTAS : TC_MIN_CTAS32_1W);
+  return (const void*)batch_kernel<NC, G, minb, TAPS>;
 }
 template <int NC, int G>
 const void* rollout_fn() { return (const void*)rollout_kernel<NC, G>; }
 
-const void* select_batch(int nc, int group, bool wide = false) {
+template <bool WIDE, bool TAPS>
+const void* select_batch_t(int nc, int group) {
   if (group == 16) {
-    if (wide) {
-      switch (nc) {
-        case 1: return batch_fn<1, 16, true>();
-        case 2: return batch_fn<2, 16, true>();
-        case 3: return batch_fn<3, 16, true>();
-        default: return batch_fn<4, 16, true>();
-      }
-    }
     switch (nc) {
-      case 1: return batch_fn<1, 16>();
-      case 2: return batch_fn<2, 16>();
-      case 3: return batch_fn<3, 16>();
-      default: return batch_fn<4, 16>();
+      case 1: return batch_fn<1, 16, WIDE, TAPS>();
+      case 2: return batch_fn<2, 16, WIDE, TAPS>();
+      case 3: return batch_fn<3, 16, WIDE, TAPS>();
+      default: return batch_fn<4, 16, WIDE, TAPS>();
     }
   }
   switch (nc) {
-    case 1: return batch_fn<1, 32>();
-    case 2: return batch_fn<2, 32>();
-    case 3: return batch_fn<3, 32>();
-    case 4: return batch_fn<4, 32>();
-    case 8: return batch_fn<8, 32>();
-    case 16: return batch_fn<16, 32>();
-    default: return batch_fn<32, 32>();
+    case 1: return batch_fn<1, 32, WIDE, TAPS>();
+    case 2: return batch_fn<2, 32, WIDE, TAPS>();
+    case 3: return batch_fn<3, 32, WIDE, TAPS>();
+    case 4: return batch_fn<4, 32, WIDE, TAPS>();
+    case 8: return batch_fn<8, 32, WIDE, TAPS>();
+    case 16: return batch_fn<16, 32, WIDE, TAPS>();
+    default: return batch_fn<32, 32, WIDE, TAPS>();
   }
+}
+const void* select_batch(int nc, int group, bool wide = false, bool taps = false) {
+  if (taps) return select_batch_t<true, true>(nc, group);
+  return wide ? select_batch_t<true, false>(nc, group) : select_batch_t<false, false>(nc, group);
 }
 const void* select_rollout(int nc, int group) {
   if (group == 16) {
@@ -2563,12 +2672,14 @@ int launch_geometry(tc_spec* s) {
   if (d.npairs > 4) d.npairs = 4;
   d.warp_smem = warp_smem_layout(d, d.direct == 1 ? 0 : (d.mirror ? 2 * d.npairs : 2));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
+  d.stage_bytes = d.smem_map ? s->map_bytes : s->tab_bytes;
   const size_t map_bytes = (size_t)map_smem_bytes(d);
   // + the per-CTA scratch of the step kernel (actions / rewards / dones)
   s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * (32 / d.group) * d.warp_smem + CTA_SCRATCH;
   s->nc = pick_nc(d.obs_w, d.group);
-  const void* fns[3] = {select_batch(s->nc, d.group), select_rollout(s->nc, d.group),
-                        select_batch(s->nc, d.group, true)};
+  const void* fns[4] = {select_batch(s->nc, d.group), select_rollout(s->nc, d.group),
+                        select_batch(s->nc, d.group, true),
+                        select_batch(s->nc, d.group, true, true)};
   // the attribute is per function, shared by every spec: raise it to the
   // device's opt-in maximum once instead of per spec (occupancy follows the
   // smem each launch actually asks for)
@@ -2616,7 +2727,7 @@ OutDev to_dev(const tc_out* o) {
 // latency variant cannot hold them all
 bool use_wide(const tc_spec* s, int64_t n) {
   const int per_cta = WARPS_PER_CTA * (32 / s->dev.group);
-  return s->dev.group == 16 && n > (int64_t)s->max_ctas * per_cta;
+  return n > (int64_t)s->max_ctas * per_cta;
 }
 
 int grid_for(const tc_spec* s, int64_t n, bool wide = false) {
@@ -2638,6 +2749,17 @@ extern "C" {
 int tc_abi_version(void) { return TC_ABI_VERSION; }
 
 // perf-experiment hook: per-env phase timestamps (TC_TRACE builds only)
+int tc_debug_trace_cta(void* dev_buf) {
+#if TC_TRACE
+  TC_CUDA(cudaMemcpyToSymbol(g_trace_cta, &dev_buf, sizeof(void*)));
+  static unsigned int zeros[16384] = {0};
+  TC_CUDA(cudaMemcpyToSymbol(g_cta_gen, zeros, sizeof zeros));
+  return TC_OK;
+#else
+  (void)dev_buf;
+  return fail(TC_E_INVALID, "library built without TC_TRACE");
+#endif
+}
 int tc_debug_trace(void* dev_buf) {
 #if TC_TRACE
   TC_CUDA(cudaMemcpyToSymbol(g_trace, &dev_buf, sizeof(void*)));
@@ -2664,24 +2786,30 @@ int tc_spec_create(const tc_tables* t, tc_spec** out) {
   for (int p = 0; p < t->n_pal; p++) pal[p] = pack_rgb(t->pal + 3 * p);
   for (int d = 0; d < t->n_doors; d++) doorrgb[d] = pack_rgb(t->door_rgb + 3 * t->dcol[d]);
 
+  // blob: the small read-only tables first (always staged into shared
+  // memory), then the packed cells and the guarded stop codes (staged when
+  // the map fits, SpecDev::stage_bytes)
   BlobBuilder b;
+  const size_t o_coef = b.add(t->coef, t->obs_w * 8);
+  const size_t o_pal = b.add(pal.data(), pal.size() * 4);
+  const size_t o_door = b.add(doorrgb.data(), doorrgb.size() * 4);
+  const size_t o_epx = b.add(t->epx, t->n_entities * 8);
+  const size_t o_epy = b.add(t->epy, t->n_entities * 8);
+  const size_t o_spx = b.add(t->spx, t->n_spawns * 8);
+  const size_t o_spy = b.add(t->spy, t->n_spawns * 8);
+  const size_t o_goal = b.add(t->goal_ent, t->n_goals * 4);
+  const size_t o_dcol = b.add(t->dcol, t->n_doors);
+  const size_t o_dlock = b.add(t->dlock, t->n_doors);
+  const size_t o_ekind = b.add(t->ekind, t->n_entities);
+  const size_t o_ecol = b.add(t->ecol, t->n_entities);
+  const size_t tab_end = (b.bytes.size() + 15) & ~(size_t)15;
   const size_t o_cell = b.add(cells.data(), cells.size() * 4);
   // stop codes with a wall guard of w+1 cells on each side (speculative DDA)
   std::vector<uint32_t> gsolid(solid.size() + 2 * (size_t)(t->w + 1), 0xffffffffu);
   std::copy(solid.begin(), solid.end(), gsolid.begin() + (t->w + 1));
   const size_t o_solid = b.add(gsolid.data(), gsolid.size() * 4) + (size_t)(t->w + 1) * 4;
-  const size_t o_pal = b.add(pal.data(), pal.size() * 4);
-  const size_t o_door = b.add(doorrgb.data(), doorrgb.size() * 4);
-  const size_t o_dcol = b.add(t->dcol, t->n_doors);
-  const size_t o_dlock = b.add(t->dlock, t->n_doors);
-  const size_t o_epx = b.add(t->epx, t->n_entities * 8);
-  const size_t o_epy = b.add(t->epy, t->n_entities * 8);
-  const size_t o_ekind = b.add(t->ekind, t->n_entities);
-  const size_t o_ecol = b.add(t->ecol, t->n_entities);
-  const size_t o_spx = b.add(t->spx, t->n_spawns * 8);
-  const size_t o_spy = b.add(t->spy, t->n_spawns * 8);
-  const size_t o_goal = b.add(t->goal_ent, t->n_goals * 4);
-  const size_t o_coef = b.add(t->coef, t->obs_w * 8);
+  const size_t map_end = (b.bytes.size() + 15) & ~(size_t)15;
+  b.bytes.resize(map_end, 0);
 
   tc_spec* s = new tc_spec();
   cudaError_t e = cudaMalloc(&s->blob, b.bytes.size());
@@ -2705,6 +2833,14 @@ int tc_spec_create(const tc_tables* t, tc_spec** out) {
   d.spy = (const double*)(base + o_spy);
   d.goal_ent = (const int32_t*)(base + o_goal);
   d.coef = (const double*)(base + o_coef);
+  d.blob = base;
+  d.b_coef = (int)o_coef; d.b_pal = (int)o_pal; d.b_door = (int)o_door;
+  d.b_epx = (int)o_epx; d.b_epy = (int)o_epy; d.b_spx = (int)o_spx; d.b_spy = (int)o_spy;
+  d.b_goal = (int)o_goal; d.b_dcol = (int)o_dcol; d.b_dlock = (int)o_dlock;
+  d.b_ekind = (int)o_ekind; d.b_ecol = (int)o_ecol; d.b_cell = (int)o_cell;
+  d.b_solid = (int)o_solid;
+  s->tab_bytes = (int)tab_end;
+  s->map_bytes = (int)map_end;
   for (int k = 0; k < FC_COUNT; k++) d.fc[k] = t->fc[k];
   for (int k = 0; k < 8; k++) d.dirs[k] = t->dirs[k];
   d.max_steps = t->ic[0];
@@ -2761,7 +2897,8 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
   OutDev od = to_dev(out);
   od.res_host = res_host;
   od.flag_host = flag_host;
-  const bool wide = use_wide(s, n);
+  const bool taps = out->zbuf || out->rayinfo || out->spritevis;
+  const bool wide = taps || use_wide(s, n);
   const int grid = grid_for(s, n, wide);
   const long long nn = n;
   const long long* acts = reinterpret_cast<const long long*>(actions_dev);
@@ -2778,7 +2915,7 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TC_CUDA(cudaLaunchKernelExC(&cfg, select_batch(s->nc, s->dev.group, wide), args));
+  TC_CUDA(cudaLaunchKernelExC(&cfg, select_batch(s->nc, s->dev.group, wide, taps), args));
   return TC_OK;
 }
 

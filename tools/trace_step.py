@@ -50,3 +50,18 @@ hist = np.histogram(rel[:, 0], bins=8)
 print("  start-time histogram (us):", [f"{e:.0f}" for e in hist[1]], hist[0].tolist())
 hist = np.histogram(rel[:, 5], bins=8)
 print("  end-time histogram (us):", [f"{e:.0f}" for e in hist[1]], hist[0].tolist())
+info = t[:, 7]
+m = info & 0xFF
+px = info >> 8
+print("  by sprites drawn (m): env total us mean / max, count")
+for k in range(0, int(m.max()) + 1):
+    sel = m == k
+    if sel.any():
+        print(f"    m={k}: {tot[sel].mean():6.2f} / {tot[sel].max():6.2f}  n={int(sel.sum())}"
+              f"  sprite px mean {px[sel].mean():.0f}  compose+sprites mean "
+              f"{(rel[sel, 5] - rel[sel, 4]).mean():.2f}  setup mean {(rel[sel, 4] - rel[sel, 3]).mean():.2f}")
+slow = np.argsort(-tot)[:12]
+print("  slowest envs: total, phases (load,dyn,walls,sprites,compose), m, px")
+for i in slow:
+    ph = np.diff(rel[i, :6])
+    print(f"    env {i:5d}: {tot[i]:6.2f}  {np.round(ph, 2).tolist()}  m={int(m[i])} px={int(px[i])}")
