@@ -2170,15 +2170,23 @@ __device__ __forceinline__ void store_env(const SpecDev& S, const StateDev& st, 
 // shared memory at the same offsets, so every table read on the step's
 // critical path is a shared-memory load instead of an L1/L2 round trip.
 __host__ __device__ __forceinline__ int map_smem_bytes(const SpecDev& S) { return S.stage_bytes; }
+// The copy itself is one TMA bulk copy (cp.async.bulk global -> shared,
+// completion counted in bytes on an mbarrier) issued by thread 0: one
+// instruction instead of a per-thread loop of 16-byte cp.async chunks.
+__shared__ __align__(8) uint64_t g_stage_bar;
+
 __device__ __forceinline__ void stage_map_issue(const SpecDev& S, uint32_t* smap,
                                                 const uint32_t*& cell, const uint32_t*& solid) {
-  // the blob prefix -> shared memory at the same offsets, 16-byte cp.async
-  // chunks all in flight at once (entries are 16-byte aligned and padded)
-  const int n4 = S.stage_bytes >> 4;
-  const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(smap);
-  for (int k = threadIdx.x; k < n4; k += blockDim.x) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16u * k),
-                 "l"(S.blob + 16 * k) : "memory");
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&g_stage_bar);
+  if (threadIdx.x == 0) {
+    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(smap);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((uint32_t)S.stage_bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(sdst), "l"(S.blob), "r"((uint32_t)S.stage_bytes), "r"(bar) : "memory");
   }
   if (S.smem_map) {
     cell = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(smap) + S.b_cell);
@@ -2188,9 +2196,18 @@ __device__ __forceinline__ void stage_map_issue(const SpecDev& S, uint32_t* smap
     solid = S.solid;
   }
 }
+// every thread: the barrier is initialised (CTA barrier), then its phase 0
+// completes when the bulk copy's bytes have landed
 __device__ __forceinline__ void stage_map_wait() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&g_stage_bar);
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra WAIT%=;\n\t"
+      "}" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, const uint32_t*& cell,
                                           const uint32_t*& solid) {
@@ -2462,6 +2479,14 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   const int grp = threadIdx.x >> 5;
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
   const uint32_t *cell, *solid;
+#if TC_TRACE
+  unsigned long long tcta[4] = {0, 0, 0, 0};
+  unsigned int tgen = 0;
+  if (g_trace_cta && threadIdx.x == 0) {
+    tcta[0] = gtime();
+    tgen = atomicAdd(&g_cta_gen[blockIdx.x], 1u);
+  }
+#endif
   asm volatile("griddepcontrol.launch_dependents;");
   const long long n = ls.n;
   const long long cbase = ONE_WAVE ? (long long)blockIdx.x * ls.epc : 0;
@@ -2470,14 +2495,19 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   long long i = ONE_WAVE ? (grp < cta_envs ? cbase + grp : n)
                          : (long long)grp * gridDim.x + blockIdx.x;
   const int map_bytes = map_smem_bytes(S);
-  uint8_t* cta_s = smem + map_bytes + WARPS_PER_CTA * S.warp_smem;
   // mapped host path: the host wrote the actions before the launch (see
   // batch_kernel); device actions are read after griddepcontrol.wait
   long long act = 0;
   if (ls.early && i < n) act = actions[i];
   stage_map_issue(S, smap, cell, solid);
   stage_map_wait();
+#if TC_TRACE
+  if (g_trace_cta && threadIdx.x == 0) tcta[1] = gtime();
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#if TC_TRACE
+  if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
+#endif
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   constexpr size_t FB = (size_t)FW * FH * 3;
   const size_t frame_bytes = FB ? FB : (size_t)S.obs_h * S.obs_w * 3;
@@ -2489,61 +2519,95 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     if (!(ls.early && first)) act = actions[i];
     first = false;
     Env e;
+    TRACE(i, 0);
     load_env<G>(S, st, i, e);
-    int status = TC_ST_OK;
-    uint32_t viol = 0;
-    double reward = 0.0;
-    int done = 0;
+    // outputs, status and host results are written as soon as they are
+    // known, so nothing but the env index stays live across the render
     if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
-      status = TC_ST_BAD_ACTION;
-      if (out.flag_host && lane == 0) *(volatile int32_t*)out.flag_host = 1;
       store_env<G>(S, so, i, e);  // out-of-place: carry the state over
+      if (lane == 0) {
+        out.statuses[i] = TC_ST_BAD_ACTION;
+        if (out.flag_host) {
+          *(volatile int32_t*)out.flag_host = 1;
+        } else if (counters) {
+          atomicOr(&counters->bad_status, 1u << TC_ST_BAD_ACTION);
+        }
+        if (ONE_WAVE && out.res_host) {  // a voided env reports reward 0, done 0
+          reinterpret_cast<double*>(out.res_host)[i] = 0.0;
+          out.res_host[(size_t)n * 8 + i] = 0;
+        }
+      }
     } else {
+      TRACE(i, 1);
       const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
       if (lane == 0) {
         out.rewards[i] = o.reward;
         out.dones[i] = (uint8_t)o.done;
         out.truncs[i] = (uint8_t)o.trunc;
         out.events[i] = o.events;
+        out.statuses[i] = TC_ST_OK;
+        if (o.violation && counters)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&counters->violations), 1ull);
+        if (ONE_WAVE && out.res_host) {
+          // this env's [reward | done] straight to pinned host memory (the
+          // CTA's envs are contiguous: the warps' stores merge on the bus)
+          reinterpret_cast<double*>(out.res_host)[i] = o.reward;
+          out.res_host[(size_t)n * 8 + i] = (uint8_t)o.done;
+        }
       }
-      reward = o.reward;
-      done = o.done;
-      viol = (uint32_t)o.violation;
       if (o.done && auto_reset) reset_draws(S, e);
       store_env<G>(S, so, i, e);
+      TRACE(i, 2);
       uint8_t* frame = out.frames + (size_t)i * frame_bytes;
       const double planex = -e.dy * PLANE_HALF_WIDTH;
       const double planey = e.dx * PLANE_HALF_WIDTH;
       const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h &&
                           (e.dx != 0.0 || e.dy != 0.0);
-      status = inside ? wall_pass<NC, false, G, true>(S, cell, solid, sm, e, planex, planey,
-                                                      nullptr, nullptr)
-                      : wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, nullptr,
-                                              nullptr, false);
+      int status;
+      if (inside) {
+        wall_pass<NC, false, G, true>(S, cell, solid, sm, e, planex, planey, nullptr, nullptr);
+        status = TC_ST_OK;
+      } else {
+        status = wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, nullptr, nullptr,
+                                       false);
+      }
       __syncwarp();
+      TRACE(i, 3);
       if (status == TC_ST_OK) {
         const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
+        TRACE(i, 4);
+#if TC_TRACE
+        if (g_trace && lane == 0) g_trace[i * 8 + 7] = (unsigned long long)m;
+#endif
         if constexpr (FW != 0) mirror_contig_fixed<FW, FH, G>(S, sm, m, frame);
         else mirror_contig<NC, G>(S, sm, m, frame);
+      } else if (lane == 0) {
+        out.statuses[i] = status;
+        if (counters) atomicOr(&counters->bad_status, 1u << status);
       }
     }
-    if (lane == 0) {
-      out.statuses[i] = status;
-      if (counters) {
-        if (viol) atomicAdd(reinterpret_cast<unsigned long long*>(&counters->violations), 1ull);
-        if (status != TC_ST_OK && !(status == TC_ST_BAD_ACTION && out.flag_host))
-          atomicOr(&counters->bad_status, 1u << status);
-      }
-      if (ONE_WAVE && out.res_host) {
-        // this env's [reward | done] straight to pinned host memory (the
-        // CTA's envs are contiguous: the warps' stores merge on the bus)
-        reinterpret_cast<double*>(out.res_host)[i] = status == TC_ST_BAD_ACTION ? 0.0 : reward;
-        out.res_host[(size_t)n * 8 + i] = status == TC_ST_BAD_ACTION ? 0 : (uint8_t)done;
-      }
+#if TC_TRACE
+    if (g_trace && lane == 0) {
+      unsigned int smid;
+      asm("mov.u32 %0, %smid;" : "=r"(smid));
+      g_trace[i * 8 + 5] = gtime();
+      g_trace[i * 8 + 6] = smid | ((unsigned long long)grp << 16) |
+                           ((unsigned long long)blockIdx.x << 32);
     }
+#endif
     if (ONE_WAVE) break;
     i = counters ? __shfl_sync(0xffffffffu, tnext, 0) : i + ls.stride;
   }
+#if TC_TRACE
+  if (g_trace_cta) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tcta[3] = gtime();
+      unsigned long long* d = g_trace_cta + ((size_t)tgen * 16384 + blockIdx.x) * 4;
+      d[0] = tcta[0]; d[1] = tcta[1]; d[2] = tcta[2]; d[3] = tcta[3];
+    }
+  }
+#endif
   if (!ONE_WAVE && !counters) return;
   if (!ONE_WAVE || out.res_host) {
     volatile int& s_last = *reinterpret_cast<int*>(smem);
@@ -2876,6 +2940,21 @@ int device_sm_count() {
   return sms;
 }
 
+// dynamic shared memory limit of a kernel = the opt-in maximum minus its
+// static shared memory (the staging mbarrier)
+int raise_smem(const void* fn, int optin) {
+  cudaFuncAttributes fa;
+  TC_CUDA(cudaFuncGetAttributes(&fa, fn));
+  TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               optin - (int)fa.sharedSizeBytes));
+  return TC_OK;
+}
+#define TC_TRY_RC(x)              \
+  do {                            \
+    const int _rc = (x);          \
+    if (_rc != TC_OK) return _rc; \
+  } while (0)
+
 int launch_geometry(tc_spec* s) {
   SpecDev& d = s->dev;
   const int row_bytes = d.obs_w * 3;
@@ -2927,10 +3006,10 @@ int launch_geometry(tc_spec* s) {
   int dev = 0, optin = 0;
   TC_CUDA(cudaGetDevice(&dev));
   TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  if (s->smem_bytes > (size_t)optin)
+  if (s->smem_bytes + 64 > (size_t)optin)
     return fail(TC_E_CAPACITY, "per-CTA shared memory exceeds the device limit");
   for (const void* fn : fns)
-    TC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    TC_TRY_RC(raise_smem(fn, optin));
   int per_sm = 0;
   TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[0], WARPS_PER_CTA * 32,
                                                         s->smem_bytes));
@@ -2947,9 +3026,8 @@ int launch_geometry(tc_spec* s) {
            32 % (d.obs_w / 16) == 0;
   if (d.lean) {
     const void* lf = select_lean(d.obs_w, d.obs_h, true);
-    TC_CUDA(cudaFuncSetAttribute(lf, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    TC_CUDA(cudaFuncSetAttribute(select_lean(d.obs_w, d.obs_h, false),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    TC_TRY_RC(raise_smem(lf, optin));
+    TC_TRY_RC(raise_smem(select_lean(d.obs_w, d.obs_h, false), optin));
     s->lean_smem = map_bytes + (size_t)WARPS_PER_CTA * d.warp_smem + CTA_SCRATCH;
     TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lf, WARPS_PER_CTA * 32,
                                                           s->lean_smem));

@@ -33,11 +33,20 @@ buf = torch.zeros((K + 3, 16384, 4), dtype=torch.int64, device=dev)
 for s in range(3):
     launch_batch(bs._ds, bs._sb, acts[s], outs[s], n, L.MODE_STEP, True, False, bs._counters)
 torch.cuda.synchronize()
+# the K launches are captured into a CUDA graph like bench.py's timed region
+# (a Python launch loop would be CPU-bound and hide the device-side gaps)
+graph = torch.cuda.CUDAGraph()
+cap = torch.cuda.Stream(dev)
+cap.wait_stream(torch.cuda.current_stream(dev))
+with torch.cuda.stream(cap):
+    with torch.cuda.graph(graph, stream=cap):
+        for s in range(K):
+            launch_batch(bs._ds, bs._sb, acts[3 + s], outs[3 + s], n, L.MODE_STEP, True, False,
+                         bs._counters)
+torch.cuda.synchronize()
 N.check(lib.tc_debug_trace_cta(buf.data_ptr()), "trace_cta")
 torch.cuda.synchronize()
-for s in range(K):
-    launch_batch(bs._ds, bs._sb, acts[3 + s], outs[3 + s], n, L.MODE_STEP, True, False,
-                 bs._counters)
+graph.replay()
 torch.cuda.synchronize()
 t = buf.cpu().numpy()[:K].astype(np.int64)
 used = (t[:, :, 3] > 0).all(axis=0)   # CTAs that ran an env in every launch
