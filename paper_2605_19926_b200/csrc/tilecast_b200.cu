@@ -232,7 +232,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #define TRACE(i, slot)                                                   \
   do {                                                                   \
-    if (g_trace && (threadIdx.x & (G - 1)) == 0) g_trace[(i) * 8 + (slot)] = gtime(); \
+    if (g_trace && (threadIdx.x & (G - 1)) == 0) g_trace[(i) * 16 + (slot)] = gtime(); \
   } while (0)
 #else
 #define TRACE(i, slot) do { } while (0)
@@ -663,6 +663,28 @@ __device__ inline WarpSmem carve(uint8_t* base) {
 }
 
 
+// (int)min(H / perp, 1e9) // 2 (_pycore.py:171-174) with the IEEE division
+// replaced on the common path: q = H * r, r = rcp.approx refined by two
+// Newton steps (relative error < 2^-50), is within q * 2^-49 of H / perp,
+// and fl(H / perp) within q * 2^-53 of it; when q is farther than
+// q * 2^-40 from an integer, floor(q) = floor(fl(H / perp)) exactly.
+// Near-integers, q >= 1e9 - 1 and non-finite values take the division.
+__device__ __forceinline__ int line_half(int H, double perp) {
+  double r0;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(perp));
+  const double e0 = fma(-perp, r0, 1.0);
+  const double r1 = fma(r0, e0, r0);
+  const double e1 = fma(-perp, r1, 1.0);
+  const double r2 = fma(r1, e1, r1);
+  const double q = (double)H * r2;
+  const double fq = floor(q);
+  const double tol = q * 0x1p-40;
+  if (q < 999999999.0 && q - fq > tol && (fq + 1.0) - q > tol) return (int)fq / 2;
+  double lh_f = (double)H / perp;
+  if (lh_f > 1e9) lh_f = 1e9;
+  return (int)lh_f / 2;
+}
+
 // One DDA march, _pycore.py:38-96. `solid` holds per-cell stop codes
 // (wall = ~0u, door d = 1u << d, floor = 0): a ray stops in a cell iff
 // (code & ~dmask) != 0 or code == ~0u (walls, closed doors). With a sealed
@@ -747,22 +769,19 @@ struct RaySetup {
 };
 __device__ __forceinline__ RaySetup ray_setup(int mw, double ox, double oy, int mapx0, int mapy0,
                                               double rx, double ry) {
+  // _pycore.py:44-63 without branches: __drcp_rn is the IEEE reciprocal (the
+  // exact 1.0 / r, inf for a zero component), the axis with a zero
+  // component gets sdx = inf and step 0 like the reference; a NaN component
+  // takes the reference's r < 0 arm (step -1)
   RaySetup r;
-  int stepy;
-  if (rx != 0.0) {
-    r.ddx = fabs(1.0 / rx);
-    r.stepx = rx > 0.0 ? 1 : -1;
-    r.sdx = rx > 0.0 ? (((double)mapx0 + 1.0) - ox) * r.ddx : (ox - (double)mapx0) * r.ddx;
-  } else {
-    r.ddx = dinf(); r.stepx = 0; r.sdx = dinf();
-  }
-  if (ry != 0.0) {
-    r.ddy = fabs(1.0 / ry);
-    stepy = ry > 0.0 ? 1 : -1;
-    r.sdy = ry > 0.0 ? (((double)mapy0 + 1.0) - oy) * r.ddy : (oy - (double)mapy0) * r.ddy;
-  } else {
-    r.ddy = dinf(); stepy = 0; r.sdy = dinf();
-  }
+  r.ddx = fabs(__drcp_rn(rx));
+  r.stepx = rx > 0.0 ? 1 : (rx != 0.0 ? -1 : 0);
+  const double fx = rx > 0.0 ? (((double)mapx0 + 1.0) - ox) : (ox - (double)mapx0);
+  r.sdx = rx != 0.0 ? fx * r.ddx : dinf();
+  r.ddy = fabs(__drcp_rn(ry));
+  const int stepy = ry > 0.0 ? 1 : (ry != 0.0 ? -1 : 0);
+  const double fy = ry > 0.0 ? (((double)mapy0 + 1.0) - oy) : (oy - (double)mapy0);
+  r.sdy = ry != 0.0 ? fy * r.ddy : dinf();
   r.dyi = stepy * mw;
   r.idx = mapy0 * mw + mapx0;
   return r;
@@ -1024,31 +1043,32 @@ __device__ __forceinline__ void march_fast(uint32_t smask, FastRay (&a)[R]) {
 // Wall pass: lane L casts the rays of columns L + 32j; per-column spans,
 // colours and zbuf go to shared memory (_pycore.py:153-190). Returns the
 // status of the first failing column (warp-uniform).
-template <int NC, bool CHECKED, int G, bool FAST = false>
+template <int NC, bool CHECKED, int G, bool FAST = false, int FWC = 0, int FHC = 0>
 __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __restrict__ cell,
                                          const uint32_t* __restrict__ solid,
                                          const WarpSmem& sm, const Env& e, double planex,
                                          double planey, double* __restrict__ zbuf_out,
-                                         int32_t* __restrict__ rayinfo) {
+                                         int32_t* __restrict__ rayinfo, long long ti = -1) {
   const Grp<G> g;
   const int lane = g.lane;
-  const int W = S.obs_w, H = S.obs_h, h2 = H / 2, mw = S.w;
+  // (FWC / FHC: compile-time frame shape -- the column rounds unroll)
+  const int W = FWC ? FWC : S.obs_w, H = FHC ? FHC : S.obs_h, h2 = H / 2, mw = S.w;
   const int ox = (int)floor(e.x), oy = (int)floor(e.y);
   const double atten = S.fc[FC_ATTEN];
   int bad_col = 0x7fffffff, bad_status = TC_ST_OK;
   // the shaded wall slice of column c from its perpendicular distance and
   // hit cell (the ray state itself is dead by now)
-  auto col_write = [&](int c, double perp, int hit) {
+  // the hit cell's base colour (door colour or wall palette entry)
+  auto col_base = [&](int hit) -> uint32_t {
+    const uint32_t cw = cell[hit];
+    return (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? T_DOOR(S)[cw & 31u] : T_PAL(S)[cw & 0xffu];
+  };
+  // column c's outputs from its distance, base colour and half height;
+  // split from the loads so a lane's rays issue their loads and arithmetic
+  // back to back before any shared-memory store orders them
+  auto col_store = [&](int c, double perp, uint32_t rgb, int half) {
     sm.zbuf(S)[c] = perp;
     if (zbuf_out) zbuf_out[c] = perp;
-    const double shade = 1.0 / (1.0 + atten * perp);
-    const uint32_t cw = cell[hit];
-    const uint32_t base = (((cw >> CELL_TAG_SHIFT) & 3u) == C_DOOR) ? T_DOOR(S)[cw & 31u]
-                                                                     : T_PAL(S)[cw & 0xffu];
-    const uint32_t rgb = rgb_scale(base, shade);
-    double lh_f = (double)H / perp;
-    if (lh_f > 1e9) lh_f = 1e9;
-    const int half = (int)lh_f / 2;
     const int top = h2 - half, bot = h2 + half;
     if (S.contig) {
       // mirrored compose reads only the (colour, top) byte streams
@@ -1063,6 +1083,10 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
       sm.t8(S)[c] = (uint8_t)(top > 0 ? top : 0);
       sm.b0(S)[c] = (uint16_t)(bot < H ? bot : H);
     }
+  };
+  auto col_write = [&](int c, double perp, int hit) {
+    const uint32_t base = col_base(hit);
+    col_store(c, perp, rgb_scale(base, __drcp_rn(1.0 + atten * perp)), line_half(H, perp));
   };
   // per-column result -> zbuf / spans / shaded colour, _pycore.py:159-178
   auto column_out = [&](int c, const March& r) {
@@ -1098,7 +1122,13 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
         fr[q].incx = 4 * rs.stepx; fr[q].incy = 4 * rs.dyi;
         fr[q].last = fr[q].incx;
       }
+#if TC_TRACE
+      if (ti >= 0) TRACE(ti, 8);
+#endif
       march_fast<LR>(smask, fr);
+#if TC_TRACE
+      if (ti >= 0) TRACE(ti, 9);
+#endif
       if (rayinfo) {
 #pragma unroll
         for (int q = 0; q < LR; q++) {
@@ -1122,8 +1152,18 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
           perp[q] = xs ? fr[q].sdx - fr[q].ddx : fr[q].sdy - fr[q].ddy;
           hit[q] = (int)(fr[q].addr - sbase) >> 2;
         }
+        uint32_t base[LR], rgb[LR];
+        int half[LR];
 #pragma unroll
-        for (int q = 0; q < LR; q++) col_write(c + q * G, perp[q], hit[q]);
+        for (int q = 0; q < LR; q++) base[q] = col_base(hit[q]);
+#pragma unroll
+        for (int q = 0; q < LR; q++) {
+          // shade = 1.0 / (1.0 + atten * perp) (IEEE reciprocal), _pycore.py:161-170
+          rgb[q] = rgb_scale(base[q], __drcp_rn(1.0 + atten * perp[q]));
+          half[q] = line_half(H, perp[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < LR; q++) col_store(c + q * G, perp[q], rgb[q], half[q]);
       }
     };
     constexpr int LR = TC_LOCKSTEP;
@@ -2107,7 +2147,7 @@ __device__ __forceinline__ int render_env(const SpecDev& S, const uint32_t* __re
       const double w = 2.0 * r.halfk * (S.obs_w - 1) / 2.0;
       px += (unsigned long long)(r.r1 - r.r0) * (unsigned long long)(w < S.obs_w ? w : S.obs_w);
     }
-    g_trace[ti * 8 + 7] = (unsigned long long)m | (px << 8);
+    g_trace[ti * 16 + 7] = (unsigned long long)m | (px << 8);
   }
 #endif
   render_frame_out<NC, G, FIX>(S, sm, m, frame, bulk_pending, buf, lg);
@@ -2373,8 +2413,8 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     if (g_trace && lane == 0) {
       unsigned int smid;
       asm("mov.u32 %0, %smid;" : "=r"(smid));
-      g_trace[i * 8 + 5] = gtime();
-      g_trace[i * 8 + 6] = smid | ((unsigned long long)grp << 16) |
+      g_trace[i * 16 + 5] = gtime();
+      g_trace[i * 16 + 6] = smid | ((unsigned long long)grp << 16) |
                            ((unsigned long long)blockIdx.x << 32);
     }
 #endif
@@ -2565,7 +2605,8 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
                           (e.dx != 0.0 || e.dy != 0.0);
       int status;
       if (inside) {
-        wall_pass<NC, false, G, true>(S, cell, solid, sm, e, planex, planey, nullptr, nullptr);
+        wall_pass<NC, false, G, true, FW, FH>(S, cell, solid, sm, e, planex, planey, nullptr,
+                                              nullptr, TC_TRACE ? i : -1);
         status = TC_ST_OK;
       } else {
         status = wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, nullptr, nullptr,
@@ -2577,7 +2618,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
         const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
         TRACE(i, 4);
 #if TC_TRACE
-        if (g_trace && lane == 0) g_trace[i * 8 + 7] = (unsigned long long)m;
+        if (g_trace && lane == 0) g_trace[i * 16 + 7] = (unsigned long long)m;
 #endif
         if constexpr (FW != 0) mirror_contig_fixed<FW, FH, G>(S, sm, m, frame);
         else mirror_contig<NC, G>(S, sm, m, frame);
@@ -2590,8 +2631,8 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     if (g_trace && lane == 0) {
       unsigned int smid;
       asm("mov.u32 %0, %smid;" : "=r"(smid));
-      g_trace[i * 8 + 5] = gtime();
-      g_trace[i * 8 + 6] = smid | ((unsigned long long)grp << 16) |
+      g_trace[i * 16 + 5] = gtime();
+      g_trace[i * 16 + 6] = smid | ((unsigned long long)grp << 16) |
                            ((unsigned long long)blockIdx.x << 32);
     }
 #endif

@@ -21,7 +21,7 @@ spec = bench.make_spec(cfg)
 dev = torch.device("cuda", 0)
 bs = tc.batch_reset(spec, n, 0, device=dev)
 out = DeviceOut.alloc(n, spec.obs_height, spec.obs_width, dev)
-tr = torch.zeros((n, 8), dtype=torch.int64, device=dev)
+tr = torch.zeros((n, 16), dtype=torch.int64, device=dev)
 lib = N.lib()
 lib.tc_debug_trace.argtypes = [C.c_void_p]
 for s in range(4):
@@ -48,6 +48,13 @@ cnt = np.bincount(sm)
 print("  envs per SM: min", cnt[cnt > 0].min(), "max", cnt.max(), "SMs used", (cnt > 0).sum())
 hist = np.histogram(rel[:, 0], bins=8)
 print("  start-time histogram (us):", [f"{e:.0f}" for e in hist[1]], hist[0].tolist())
+if (t[:, 8] > 0).all():
+    rs = (t[:, 8] - t[:, 2]) / 1000.0
+    mr = (t[:, 9] - t[:, 8]) / 1000.0
+    cw = (t[:, 3] - t[:, 9]) / 1000.0
+    for nm, d in (("dyn->raysetup", rs), ("march", mr), ("colwrite", cw)):
+        print(f"  {nm:>17s}  mean {d.mean():7.2f} us  p50 {np.median(d):7.2f}  "
+              f"p90 {np.percentile(d, 90):7.2f}  max {d.max():7.2f}")
 hist = np.histogram(rel[:, 5], bins=8)
 print("  end-time histogram (us):", [f"{e:.0f}" for e in hist[1]], hist[0].tolist())
 info = t[:, 7]
