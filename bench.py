@@ -41,8 +41,8 @@ CONFIGS = {
     "c3": ("key-door", {}, 16384, "key-door, 16384 envs/GPU, 64x64 RGB, sprites/doors"),
     "c4": ("dmlab-static-03", {"obs_width": 128, "obs_height": 128}, 8192,
            "dmlab-static-03, 8192 envs/GPU, 128x128 RGB"),
-    "c5": ("synthetic", {}, 131072,
-           "synthetic random 6-14 tile maps, 64x64 RGB, 2^20 envs over 8 GPUs"),
+    "c5": ("synthetic", {}, 1 << 20,
+           "synthetic random 6-14 tile map, 64x64 RGB, 2^20 envs split over the GPUs"),
 }
 METRIC = "env steps/sec (rendered frames/sec) at 4096+ envs/GPU on 1/2/4/8 B200"
 L2_BYTES = 126 * 2**20
@@ -57,6 +57,40 @@ def synthetic_spec(obs=(64, 64)):
                       goal_mode=tc.GoalMode.RANDOM_PER_EPISODE, max_steps=500,
                       obs_width=obs[0], obs_height=obs[1], living_reward=0.01,
                       health_decay=0.25, health_restore=10.0)
+
+
+def physical_cores() -> int:
+    """Physical cores of this host (the CPU reference runs
+    one OpenMP thread per physical core)."""
+    try:
+        import psutil
+        n = psutil.cpu_count(logical=False)
+        if n:
+            return int(n)
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def totals(cfg: str, world: int) -> tuple[int, str]:
+    """(envs in the whole job, scaling): c2-c4 fix the envs per GPU (weak
+    scaling); c5 splits 2^20 envs over the GPUs at every N (strong)."""
+    if CONFIGS[cfg][0] == "synthetic":
+        return 1 << 20, "strong"
+    return CONFIGS[cfg][2] * world, "weak"
+
+
+def config_dict(cfg: str, spec, n: int, n_total: int, world: int) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": CONFIGS[cfg][3], "env": spec.id, "envs_per_gpu": n,
+            "envs_total": n_total, "obs": [spec.obs_width, spec.obs_height],
+            "auto_reset": True, "parallelism": f"env-shard x{world}"}
+
+
+def source_sha16() -> str:
+    import hashlib
+    src = ROOT / "paper_2605_19926_b200" / "csrc" / "tilecast_b200.cu"
+    return hashlib.sha256(src.read_bytes()).hexdigest()[:16]
 
 
 def make_spec(cfg):
@@ -166,8 +200,8 @@ def cpu_baseline(cfg, budget_s=12.0):
     sample of the workload (same spec, same env count, a few steps)."""
     import paper_2605_19926_b200 as tc
     spec = make_spec(cfg)
-    n = CONFIGS[cfg][2]
-    cores = os.cpu_count() or 1
+    n = CONFIGS[cfg][2] if CONFIGS[cfg][0] != "synthetic" else 131072
+    cores = physical_cores()
     ref_dir = ROOT / "oracle" / "_ref"
     kind = "port"
     if (ref_dir / "tilecast" / "backend").exists() and CONFIGS[cfg][0] != "synthetic":
@@ -206,7 +240,7 @@ def cpu_baseline(cfg, budget_s=12.0):
         el = time.perf_counter() - t0
     return {"value": n * steps / el, "unit": "env-steps/s", "cores": cores, "kind": kind,
             "sample": f"{CONFIGS[cfg][3]}: {n} envs x {steps} batch_step calls "
-                      f"({el:.1f} s wall, host threads={cores})"}
+                      f"({el:.1f} s wall, host threads={cores} = physical cores)"}
 
 
 def run_reference(args, rank, world):
@@ -216,10 +250,14 @@ def run_reference(args, rank, world):
     cfg = args.config
     import paper_2605_19926_b200 as tc
     spec = make_spec(cfg)
-    n = CONFIGS[cfg][2]
-    cores = os.cpu_count() or 1
+    n_total, scaling = totals(cfg, world)
+    n = n_total // world if scaling == "strong" else CONFIGS[cfg][2]
+    # the host steps the whole job's envs (a bounded 131072-env sample of the
+    # 2^20-env c5 job: its rate is flat in N once N >> threads)
+    n_run = min(n_total, 131072) if CONFIGS[cfg][0] == "synthetic" else n_total
+    cores = physical_cores()
     ref_dir = ROOT / "oracle" / "_ref"
-    acts = tc.policy_actions(spec, n, args.warmup + args.steps, 0)
+    acts = tc.policy_actions(spec, n_run, args.warmup + args.steps, 0)
     kind = "port"
     stepper = None
     if (ref_dir / "tilecast" / "backend").exists() and CONFIGS[cfg][0] != "synthetic":
@@ -229,7 +267,7 @@ def run_reference(args, rank, world):
             from tilecast import backend as rb
             from tilecast.batch import batch_reset, batch_step
             rb.set_backend("compiled")
-            bs = [batch_reset(ref.make_env(CONFIGS[cfg][0], **CONFIGS[cfg][1]), n, 0,
+            bs = [batch_reset(ref.make_env(CONFIGS[cfg][0], **CONFIGS[cfg][1]), n_run, 0,
                               n_threads=cores)]
 
             def stepper(a):
@@ -239,7 +277,7 @@ def run_reference(args, rank, world):
             stepper = None
     if stepper is None:
         from oracle import oracle as orc
-        r = orc.Rollout(spec, n, 0, n_threads=cores)
+        r = orc.Rollout(spec, n_run, 0, n_threads=cores)
         stepper = r.step
     for s in range(args.warmup):
         stepper(acts[s])
@@ -247,16 +285,16 @@ def run_reference(args, rank, world):
     for s in range(args.steps):
         stepper(acts[args.warmup + s])
     el = time.perf_counter() - t0
-    v = n * args.steps / el
+    v = n_run * args.steps / el
     line = {
         "metric": METRIC, "value": v, "unit": "env-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded uniform-random policy actions)", "impl": "reference",
-        "config": {"workload": CONFIGS[cfg][3], "env": CONFIGS[cfg][0], "envs": n,
-                   "obs": [spec.obs_width, spec.obs_height]},
+        "config": config_dict(cfg, spec, n, n_total, world),
         "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": cores, "kind": kind,
-                         "sample": f"{n} envs x {args.steps} timed batch_step calls"},
+                         "sample": f"{n_run} envs x {args.steps} timed batch_step calls on "
+                                   f"{cores} host threads (one per physical core)"},
         "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -288,6 +326,7 @@ def main():
 
     import paper_2605_19926_b200 as tc
     from paper_2605_19926_b200 import layout as L
+    from paper_2605_19926_b200 import _native as N
     from paper_2605_19926_b200.engine import DeviceOut, launch_batch
 
     # one process per GPU; TILECAST_DIST_BACKEND=gloo lets a test run several
@@ -307,12 +346,10 @@ def main():
 
     spec = make_spec(args.config)
     # c2-c4: fixed envs per GPU (weak scaling); c5: 2^20 envs in total split
-    # over the GPUs (strong scaling) -- 131072 on one GPU keeps it in minutes
-    n_cfg = CONFIGS[args.config][2]
-    n_total = (1 << 20) if (args.config == "c5" and world > 1) else n_cfg * world
+    # over the GPUs at every N (strong scaling, 1 -> 8 on the same job)
+    n_total, scaling = totals(args.config, world)
     sh = shard_range(n_total, world, rank)
     n, base = sh.n, sh.base
-    scaling = "strong" if (args.config == "c5" and world > 1) else "weak"
     H, W = spec.obs_height, spec.obs_width
     frame_bytes = n * H * W * 3
     ring = max(2, -(-2 * L2_BYTES // frame_bytes))  # >= 2x L2 of frame blocks
@@ -412,11 +449,18 @@ def main():
     write_peak = measure_write_peak(dev)
     mean_kernel_ms = float(np.mean(kern_ms))
     achieved = frame_bytes / (mean_kernel_ms / 1e3) / 1e9
-    traffic = None
+    # DRAM bytes per launch from an ncu capture of THIS kernel source and
+    # config (profiles/ncu_traffic.json, written by tools/ncu_traffic.py from
+    # 8 consecutive ring-rotated launches with --cache-control none); null
+    # when the capture was of another build
+    traffic, traffic_src = None, "no capture of this build"
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(args.config)
+            rec = json.loads(prof.read_text()).get(args.config)
+            if rec and rec.get("source_sha16") == source_sha16() and rec.get("envs") == n:
+                traffic = rec["dram_bytes_per_launch"]
+                traffic_src = rec["capture"]
         except Exception:
             traffic = None
 
@@ -428,11 +472,9 @@ def main():
             "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform-random policy actions; shipped map"
                     + (" / generated random map" if args.config == "c5" else "") + ")",
-            "config": {"workload": CONFIGS[args.config][3], "env": spec.id,
-                       "envs_per_gpu": n, "envs_total": n_total, "obs": [W, H],
-                       "auto_reset": True, "parallelism": f"env-shard x{world}",
-                       "l2": f"frame ring of {ring} output blocks "
-                             f"({ring * frame_bytes / 2**20:.0f} MiB > 2x L2)"},
+            "config": config_dict(args.config, spec, n, n_total, world),
+            "l2_policy": f"frame ring of {ring} output blocks "
+                         f"({ring * frame_bytes / 2**20:.0f} MiB > 2x L2)",
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 9,
                     "api": "batch_step_host(numpy actions, reuse=True) -> numpy rewards,"
@@ -443,7 +485,9 @@ def main():
                     "episode_stats": stats},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "batch_kernel (fused step; avg launch = graph replay / K)",
+                         "traffic_source": traffic_src,
+                         "kernel": N.lib().tc_step_kernel(bs._ds.handle, n).decode()
+                                   + "; avg launch = graph replay / K",
                          "algorithmic_bytes_per_launch": frame_bytes,
                          "mean_kernel_ms": mean_kernel_ms, "peak_source": peak_src,
                          # the kernel only writes frames: its own ceiling is the

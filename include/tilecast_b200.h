@@ -140,6 +140,9 @@ typedef struct tc_spec tc_spec; /* opaque, device-resident packed tables */
 int tc_abi_version(void);
 const char *tc_last_error(void);
 const char *tc_build_info(void);
+/* Which step kernel a tc_batch_kernel / tc_batch_step_* call over n envs of
+ * this spec launches (a description string; for reports). */
+const char *tc_step_kernel(const tc_spec *spec, int64_t n);
 
 /* Pack + upload a spec's tables once (replaces build_tables' device half,
  * tables.py:92-184). `host` points at host arrays. */

@@ -82,6 +82,7 @@ def _load() -> C.CDLL:
         "tc_abi_version": (C.c_int, []),
         "tc_last_error": (C.c_char_p, []),
         "tc_build_info": (C.c_char_p, []),
+        "tc_step_kernel": (C.c_char_p, [_p, C.c_int64]),
         "tc_spec_create": (C.c_int, [P(TcTables), P(_p)]),
         "tc_spec_destroy": (C.c_int, [_p]),
         "tc_batch_kernel": (C.c_int, [_p, P(TcState), _p, P(TcOut), C.c_int64, C.c_int32,

@@ -3148,7 +3148,22 @@ int tc_debug_trace(void* dev_buf) {
 }
 const char* tc_last_error(void) { return g_err.c_str(); }
 const char* tc_build_info(void) {
-  return "tilecast_b200 sm_100a; fp64 --fmad=false; warps/cta=4; TMA bulk-store bands";
+  return "tilecast_b200 sm_100a; fp64 --fmad=false; 4 warps/CTA; spec tables + map staged "
+         "per CTA by one TMA bulk copy (cp.async.bulk + mbarrier); one-wave steps: lean "
+         "one-env-per-warp kernel; multi-wave: two envs per warp, ticket scheduler; frames "
+         "by lane-contiguous 16-byte streaming stores (mirrored SWAR compose)";
+}
+
+const char* tc_step_kernel(const tc_spec* s, int64_t n) {
+  if (!s) return "none";
+  const SpecDev& d = s->dev;
+  if (d.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA)
+    return "lean_kernel (one env per warp, one wave, 72 registers)";
+  if (use_wide(s, n))
+    return d.group == 16 ? "batch_kernel (two envs per warp, multi-wave, 96 registers)"
+                         : "batch_kernel (one env per warp, multi-wave)";
+  return d.group == 16 ? "batch_kernel (two envs per warp, one wave, 128 registers)"
+                       : "batch_kernel (one env per warp, one wave)";
 }
 
 int tc_spec_create(const tc_tables* t, tc_spec** out) {

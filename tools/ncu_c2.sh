@@ -11,14 +11,17 @@
 # Outputs under gpurun_out/ (TAG prefix).
 CFG=${1:-c2}
 TAG=${2:-r02}
+# the step kernel: one-wave batches (c2) launch lean_kernel, multi-wave ones
+# batch_kernel (whose reset launch comes first: skip it)
+KRN=${3:-lean_kernel}
 mkdir -p gpurun_out
 B="python bench.py --config $CFG --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 5"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${TAG}_launches_${CFG}.csv $B > gpurun_out/${TAG}_ncu_launch.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_write.sum,dram__bytes_read.sum,lts__t_bytes.sum \
-  --cache-control none --clock-control none -k regex:batch_kernel --launch-skip 2 -c 8 --csv \
+  --cache-control none --clock-control none -k regex:$KRN --launch-skip 3 -c 8 --csv \
   --log-file gpurun_out/${TAG}_dram8_${CFG}.csv $B > gpurun_out/${TAG}_ncu_dram.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:batch_kernel --launch-skip 6 -c 1 \
+ncu --set full --import-source on --clock-control none -k regex:$KRN --launch-skip 6 -c 1 \
   -f -o gpurun_out/${TAG}_${CFG} $B > gpurun_out/${TAG}_ncu_full.log 2>&1
 ncu -i gpurun_out/${TAG}_${CFG}.ncu-rep --page source --csv --print-source cuda,sass \
   > gpurun_out/${TAG}_${CFG}_source.csv 2>/dev/null
