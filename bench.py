@@ -59,6 +59,15 @@ def synthetic_spec(obs=(64, 64)):
                       health_decay=0.25, health_restore=10.0)
 
 
+def clock_warm(stream, ms: float = 2.0) -> None:
+    """A short device spin (torch.cuda._sleep: one busy thread, no env work)
+    on `stream`, so the SM clock is at its under-load value when the timed
+    region starts."""
+    import torch
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(ms * 1e-3 * 1.965e9))
+
+
 def physical_cores() -> int:
     """Physical cores of this host (the CPU reference runs
     one OpenMP thread per physical core)."""
@@ -387,6 +396,11 @@ def main():
         torch.cuda.synchronize(dev)
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
+        # ~2 ms of device spin right before the timed region (no env work):
+        # the sampler's start-up and the barrier leave the GPU idle long
+        # enough for the SM clock to drop, and a 0.4 ms timed region would
+        # otherwise run partly on the ramp
+        clock_warm(stream)
         t_start.record(stream)
         graph.replay()
         t_end.record(stream)
@@ -408,6 +422,7 @@ def main():
     tc.rollout(rb, args.warmup, seed, frames=rring)
     torch.cuda.synchronize(dev)
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clock_warm(stream)
     r0.record(stream)
     tc.rollout(rb, args.steps, seed, step0=args.warmup, frames=rring)
     r1.record(stream)
@@ -429,13 +444,16 @@ def main():
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    racc = np.zeros(n)  # per-env reward sums over the timed steps
+    clock_warm(torch.cuda.current_stream(dev))
+    torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    rsum = 0.0
     for s in range(args.e2e_steps):
         eb, rh, dh = tc.batch_step_host(eb, host_acts[3 + s], reuse=True)
-        rsum += float(rh.sum())
+        np.add(racc, rh, out=racc)
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
+    rsum = float(racc.sum())
     stats = reduce_episode_stats({"reward_sum": rsum, "env_steps": n * args.e2e_steps},
                                  device=rdev)  # the optional NCCL stats reduction
     if world > 1:

@@ -2499,12 +2499,44 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
 // lean (7 CTAs of 4 warps per SM: a 4096-env batch is one wave). Envs whose
 // pose is off the grid or whose view direction is zero take the checked
 // wall pass out of line. _pycore.py:346-547 like batch_kernel.
+// Mapped host step, one wave: each warp parks its env's [reward | done] in
+// the CTA scratch right after the dynamics; at a CTA barrier warp 0 ships the
+// CTA's contiguous run to pinned host memory (one system fence per CTA) and
+// counts the CTA; the CTA completing the count raises the host's completion
+// word -- while the frames are still being rendered. The host may return
+// and prepare the next step meanwhile: anything it launches next on the
+// stream is ordered after this kernel (complete frames and state).
+__device__ __forceinline__ void ship_results(const OutDev& out, tc_counters* counters,
+                                             long long n, long long cbase, int cta_envs,
+                                             int ctas, const double* rew_s,
+                                             const uint8_t* done_s) {
+  asm volatile("bar.sync 1, %0;" ::"r"(WARPS_PER_CTA * 32) : "memory");
+  if (threadIdx.x < 32) {
+    const int k = threadIdx.x;
+    if (k < cta_envs) {
+      reinterpret_cast<double*>(out.res_host)[cbase + k] = rew_s[k];
+      out.res_host[(size_t)n * 8 + cbase + k] = done_s[k];
+    }
+    __threadfence_system();
+    __syncwarp();
+    if (k == 0) {
+      const unsigned int c = atomicAdd(&counters->ctas_done, 1u);
+      if ((int)c == ctas - 1) {
+        counters->ctas_done = 0;  // every CTA has counted: ready for the next launch
+        __threadfence_system();
+        *(volatile int32_t*)(out.flag_host + 1) = 1;
+      }
+    }
+  }
+}
+
 // Launch schedule of the lean kernel, computed on the host: one wave
 // (CTA c owns envs [c*epc, c*epc + epc)) or tickets (first env grp*grid +
 // cta, then an atomic ticket per env, stride = grid * warps per CTA).
 struct LeanSched {
   long long n, stride;
   int epc, early;
+  int ctas;  // one wave: CTAs that own envs (the mapped host step counts them)
 };
 
 template <int NC, bool ONE_WAVE, int FW, int FH>
@@ -2531,7 +2563,8 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   const long long n = ls.n;
   const long long cbase = ONE_WAVE ? (long long)blockIdx.x * ls.epc : 0;
   const int cta_envs = ONE_WAVE ? (int)max(0LL, min((long long)ls.epc, n - cbase)) : 0;
-  if ((ONE_WAVE ? cta_envs == 0 : (long long)blockIdx.x >= n) && !out.res_host) return;
+  // (multi-wave mapped steps count every CTA at the end, envs or not)
+  if (ONE_WAVE ? cta_envs == 0 : ((long long)blockIdx.x >= n && !out.res_host)) return;
   long long i = ONE_WAVE ? (grp < cta_envs ? cbase + grp : n)
                          : (long long)grp * gridDim.x + blockIdx.x;
   const int map_bytes = map_smem_bytes(S);
@@ -2549,6 +2582,12 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
 #endif
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
+  double* rew_s = reinterpret_cast<double*>(smem + map_bytes + WARPS_PER_CTA * S.warp_smem);
+  uint8_t* done_s = reinterpret_cast<uint8_t*>(rew_s + WARPS_PER_CTA);
+  // one wave, mapped: warps without an env still take part in the CTA's
+  // result hand-off barrier
+  if (ONE_WAVE && out.res_host && i >= n)
+    ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
   constexpr size_t FB = (size_t)FW * FH * 3;
   const size_t frame_bytes = FB ? FB : (size_t)S.obs_h * S.obs_w * 3;
   bool first = true;
@@ -2573,10 +2612,12 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
           atomicOr(&counters->bad_status, 1u << TC_ST_BAD_ACTION);
         }
         if (ONE_WAVE && out.res_host) {  // a voided env reports reward 0, done 0
-          reinterpret_cast<double*>(out.res_host)[i] = 0.0;
-          out.res_host[(size_t)n * 8 + i] = 0;
+          rew_s[grp] = 0.0;
+          done_s[grp] = 0;
         }
       }
+      if (ONE_WAVE && out.res_host)
+        ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
     } else {
       TRACE(i, 1);
       const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
@@ -2591,10 +2632,12 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
         if (ONE_WAVE && out.res_host) {
           // this env's [reward | done] straight to pinned host memory (the
           // CTA's envs are contiguous: the warps' stores merge on the bus)
-          reinterpret_cast<double*>(out.res_host)[i] = o.reward;
-          out.res_host[(size_t)n * 8 + i] = (uint8_t)o.done;
+          rew_s[grp] = o.reward;
+          done_s[grp] = (uint8_t)o.done;
         }
       }
+      if (ONE_WAVE && out.res_host)
+        ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
       if (o.done && auto_reset) reset_draws(S, e);
       store_env<G>(S, so, i, e);
       TRACE(i, 2);
@@ -2649,10 +2692,11 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     }
   }
 #endif
-  if (!ONE_WAVE && !counters) return;
-  if (!ONE_WAVE || out.res_host) {
+  // one wave: the host was released by results_done as soon as every env's
+  // reward / done had reached it; nothing left to count
+  if (ONE_WAVE || !counters) return;
+  {
     volatile int& s_last = *reinterpret_cast<int*>(smem);
-    if (ONE_WAVE && out.res_host && lane == 0) __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -3310,6 +3354,7 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     const bool one_wave = n <= ls.stride;
     ls.epc = one_wave ? (int)((n + grid - 1) / grid) : 0;
     ls.early = res_host != nullptr;
+    ls.ctas = one_wave ? (int)((n + ls.epc - 1) / ls.epc) : 0;
     const long long* acts = reinterpret_cast<const long long*>(actions_dev);
     int ar = auto_reset, va = validate;
     SpecDev spec = d;
