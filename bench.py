@@ -43,6 +43,11 @@ CONFIGS = {
            "dmlab-static-03, 8192 envs/GPU, 128x128 RGB"),
     "c5": ("synthetic", {}, 1 << 20,
            "synthetic random 6-14 tile map, 64x64 RGB, 2^20 envs split over the GPUs"),
+    # the large-map variant of SURVEY §8(d): 20,480 cells, beyond the 4,096
+    # staged as u32 codes -- u8 stop codes staged per CTA by one TMA bulk copy
+    "large": ("large", {}, 4096,
+              "synthetic large map 160x128 tiles (20,480 cells, TMA-staged u8 stop codes), "
+              "4096 envs/GPU, 64x64 RGB"),
 }
 METRIC = "env steps/sec (rendered frames/sec) at 4096+ envs/GPU on 1/2/4/8 B200"
 L2_BYTES = 126 * 2**20
@@ -102,10 +107,26 @@ def source_sha16() -> str:
     return hashlib.sha256(src.read_bytes()).hexdigest()[:16]
 
 
+def large_spec():
+    """The 160x128-tile map of tests/golden (large-160x128, make_golden_r2.py)."""
+    import random
+    import paper_2605_19926_b200 as tc
+    from paper_2605_19926_b200.synthetic import large_tilemap
+    tmap = large_tilemap(random.Random(13), 160, 128, n_doors=4, n_entities=16, n_spawns=16,
+                         doors_at_spawns=True)
+    return tc.EnvSpec(id="large-160x128", map=tmap, action_set=tc.suite.STRAFE_ACTIONS,
+                      goal_mode=tc.GoalMode.RANDOM_PER_EPISODE, max_steps=500,
+                      living_reward=0.01, health_decay=0.25, health_restore=10.0)
+
+
 def make_spec(cfg):
     import paper_2605_19926_b200 as tc
     env, ov, n, _ = CONFIGS[cfg]
-    return synthetic_spec() if env == "synthetic" else tc.make_env(env, **ov)
+    if env == "synthetic":
+        return synthetic_spec()
+    if env == "large":
+        return large_spec()
+    return tc.make_env(env, **ov)
 
 
 def load_peaks():
@@ -213,7 +234,7 @@ def cpu_baseline(cfg, budget_s=12.0):
     cores = physical_cores()
     ref_dir = ROOT / "oracle" / "_ref"
     kind = "port"
-    if (ref_dir / "tilecast" / "backend").exists() and CONFIGS[cfg][0] != "synthetic":
+    if (ref_dir / "tilecast" / "backend").exists() and CONFIGS[cfg][0] not in ("synthetic", "large"):
         try:
             sys.path.insert(0, str(ref_dir))
             import tilecast as ref
@@ -269,7 +290,7 @@ def run_reference(args, rank, world):
     acts = tc.policy_actions(spec, n_run, args.warmup + args.steps, 0)
     kind = "port"
     stepper = None
-    if (ref_dir / "tilecast" / "backend").exists() and CONFIGS[cfg][0] != "synthetic":
+    if (ref_dir / "tilecast" / "backend").exists() and CONFIGS[cfg][0] not in ("synthetic", "large"):
         sys.path.insert(0, str(ref_dir))
         try:
             import tilecast as ref
@@ -488,8 +509,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded uniform-random policy actions; shipped map"
-                    + (" / generated random map" if args.config == "c5" else "") + ")",
+            "data": "synthetic (seeded uniform-random policy actions; "
+                    + ("generated random map" if args.config in ("c5", "large") else "shipped map")
+                    + ")",
             "config": config_dict(args.config, spec, n, n_total, world),
             "l2_policy": f"frame ring of {ring} output blocks "
                          f"({ring * frame_bytes / 2**20:.0f} MiB > 2x L2)",

@@ -84,6 +84,7 @@ constexpr int WARPS_PER_CTA = 4;
 constexpr int BAND_BYTES_TARGET = 3072;       // per staging buffer
 constexpr int CTA_SCRATCH = 160;               // step kernel per-CTA scratch bytes
 constexpr int SMEM_MAP_MAX_CELLS = 4096;      // stage map in smem up to this
+constexpr int SMEM_U8_MAX_BYTES = 48 * 1024;  // u8 stop codes (+ tables) staged up to this
 
 // packed cell word: bits 0-7 = wall colour or door index, 8-9 = cell tag,
 // 16-23 = entity index + 1 (0 = no entity on the tile)
@@ -116,7 +117,10 @@ struct SpecDev {
   // launch geometry derived on the host
   int band_rows;     // rows per staging band
   int band_stride;   // bytes per staging buffer (16-aligned)
-  int smem_map;      // 1 = stage cells into shared memory
+  int smem_map;      // 1 = stage cells + u32 stop codes into shared memory
+  int smem_u8;       // 1 = map too large for that: stage u8 stop codes only (march in
+                     //     shared memory; cells / dynamics read global memory)
+  int b_code8;       // blob offset of the first u8 stop code (guards around it)
   int quads;         // 1 = obs_w % 4 == 0 (4-pixel packed compose)
   int bulk;          // 1 = frame rows are 16-byte multiples (TMA bulk store)
   int sealed;        // 1 = map rim is all wall (rays cannot escape)
@@ -920,6 +924,54 @@ __device__ __forceinline__ void march_fast2(uint32_t smask, FastRay& a, FastRay&
         "d"(b.ddx), "d"(b.ddy), "r"(b.incx), "r"(b.incy), "r"(smask));
 }
 
+// march_fast2 over u8 stop codes (large maps): code 0 floor, d + 1 door d
+// (n_doors <= 30), 31 wall; a ray stops iff bit `code` of `smask` is set,
+// smask = (closed doors << 1) | 1 << 31. One LDS.U8 + SHF + LOP3 per step.
+__device__ __forceinline__ void march_fast2_u8(uint32_t smask, FastRay& a, FastRay& b) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred l0, l1, x0, y0, x1, y1, any;\n\t"
+      ".reg .b32 c0, c1, ix0, iy0, ix1, iy1, sm;\n\t"
+      ".reg .f64 ex0, ey0, ex1, ey1;\n\t"
+      "mov.f64 ex0, %8;\n\t"
+      "mov.f64 ey0, %9;\n\t"
+      "mov.b32 ix0, %10;\n\t"
+      "mov.b32 iy0, %11;\n\t"
+      "mov.f64 ex1, %12;\n\t"
+      "mov.f64 ey1, %13;\n\t"
+      "mov.b32 ix1, %14;\n\t"
+      "mov.b32 iy1, %15;\n\t"
+      "mov.b32 sm, %16;\n\t"
+      "setp.eq.b32 l0, sm, sm;\n\t"
+      "setp.eq.b32 l1, sm, sm;\n\t"
+      "MARCH8%=:\n\t"
+      "setp.lt.and.f64 x0|y0, %0, %1, l0;\n\t"
+      "setp.lt.and.f64 x1|y1, %4, %5, l1;\n\t"
+      "@x0 add.rn.f64 %0, %0, ex0;\n\t"
+      "@y0 add.rn.f64 %1, %1, ey0;\n\t"
+      "@x1 add.rn.f64 %4, %4, ex1;\n\t"
+      "@y1 add.rn.f64 %5, %5, ey1;\n\t"
+      "@l0 selp.b32 %3, ix0, iy0, x0;\n\t"
+      "@l1 selp.b32 %7, ix1, iy1, x1;\n\t"
+      "@l0 add.u32 %2, %2, %3;\n\t"
+      "@l1 add.u32 %6, %6, %7;\n\t"
+      "@l0 ld.shared.u8 c0, [%2];\n\t"
+      "@l1 ld.shared.u8 c1, [%6];\n\t"
+      "@l0 shr.b32 c0, sm, c0;\n\t"
+      "@l1 shr.b32 c1, sm, c1;\n\t"
+      "@l0 and.b32 c0, c0, 1;\n\t"
+      "@l1 and.b32 c1, c1, 1;\n\t"
+      "@l0 setp.eq.b32 l0, c0, 0;\n\t"
+      "@l1 setp.eq.b32 l1, c1, 0;\n\t"
+      "or.pred any, l0, l1;\n\t"
+      "@any bra MARCH8%=;\n\t"
+      "}"
+      : "+d"(a.sdx), "+d"(a.sdy), "+r"(a.addr), "+r"(a.last),
+        "+d"(b.sdx), "+d"(b.sdy), "+r"(b.addr), "+r"(b.last)
+      : "d"(a.ddx), "d"(a.ddy), "r"(a.incx), "r"(a.incy),
+        "d"(b.ddx), "d"(b.ddy), "r"(b.incx), "r"(b.incy), "r"(smask));
+}
+
 // Four rays in lockstep (TC_LOCKSTEP=4): same loop as march_fast2; each
 // ray's x / y byte increments arrive packed as (incy << 8) | (incx & 0xff)
 // to stay within the asm operand limit.
@@ -1104,11 +1156,18 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
     col_write(c, r.xs ? r.sdx - r.ddx : r.sdy - r.ddy, r.idx);
   };
   int c = lane;
-  if (FAST || (!CHECKED && S.smem_map && S.n_doors < 32 && mw >= 2)) {
+  if (FAST || (!CHECKED && mw >= 2 &&
+                ((S.smem_map && S.n_doors < 32) || (S.smem_u8 && S.n_doors <= 30)))) {
     // shared-memory stop codes, predicated lockstep march (march_fast):
-    // rounds of TC_LOCKSTEP columns (c, c + G, ...), then pairs, then singles
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(solid);
-    const uint32_t smask = ~e.dmask;
+    // rounds of TC_LOCKSTEP columns (c, c + G, ...), then pairs, then singles.
+    // u32 codes (4-byte cells, stop iff code & ~dmask) or, for large maps,
+    // u8 codes (1-byte cells, stop iff bit `code` of the stop mask is set)
+    const bool u8 = S.smem_u8 != 0;
+    const int shift = u8 ? 0 : 2;
+    const uint32_t sbase = u8 ? (uint32_t)__cvta_generic_to_shared(g_smem + S.b_code8)
+                              : (uint32_t)__cvta_generic_to_shared(solid);
+    const uint32_t nd_mask = S.n_doors >= 32 ? ~0u : ((1u << S.n_doors) - 1u);
+    const uint32_t smask = u8 ? (((~e.dmask & nd_mask) << 1) | 0x80000000u) : ~e.dmask;
     const int idx0 = oy * mw + ox;
     auto fast_round = [&](auto rtag) {
       constexpr int LR = decltype(rtag)::value;
@@ -1118,14 +1177,19 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
         const double k = T_COEF(S)[c + q * G];
         const RaySetup rs = ray_setup(mw, e.x, e.y, ox, oy, e.dx + planex * k, e.dy + planey * k);
         fr[q].sdx = rs.sdx; fr[q].sdy = rs.sdy; fr[q].ddx = rs.ddx; fr[q].ddy = rs.ddy;
-        fr[q].addr = sbase + 4u * (uint32_t)idx0;
-        fr[q].incx = 4 * rs.stepx; fr[q].incy = 4 * rs.dyi;
+        fr[q].addr = sbase + ((uint32_t)idx0 << shift);
+        fr[q].incx = rs.stepx * (1 << shift); fr[q].incy = rs.dyi * (1 << shift);
         fr[q].last = fr[q].incx;
       }
 #if TC_TRACE
       if (ti >= 0) TRACE(ti, 8);
 #endif
-      march_fast<LR>(smask, fr);
+      if constexpr (LR == 2) {
+        if (u8) march_fast2_u8(smask, fr[0], fr[1]);
+        else march_fast<LR>(smask, fr);
+      } else {
+        march_fast<LR>(smask, fr);
+      }
 #if TC_TRACE
       if (ti >= 0) TRACE(ti, 9);
 #endif
@@ -1134,7 +1198,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
         for (int q = 0; q < LR; q++) {
           March r;
           r.sdx = fr[q].sdx; r.sdy = fr[q].sdy; r.ddx = fr[q].ddx; r.ddy = fr[q].ddy;
-          r.idx = (int)(fr[q].addr - sbase) >> 2;
+          r.idx = (int)(fr[q].addr - sbase) >> shift;
           r.xs = fr[q].last == fr[q].incx;
           r.status = TC_ST_OK;
           const int my = r.idx / mw, mx = r.idx - my * mw;
@@ -1150,7 +1214,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
         for (int q = 0; q < LR; q++) {
           const bool xs = fr[q].last == fr[q].incx;
           perp[q] = xs ? fr[q].sdx - fr[q].ddx : fr[q].sdy - fr[q].ddy;
-          hit[q] = (int)(fr[q].addr - sbase) >> 2;
+          hit[q] = (int)(fr[q].addr - sbase) >> shift;
         }
         uint32_t base[LR], rgb[LR];
         int half[LR];
@@ -1516,7 +1580,8 @@ __device__ __forceinline__ int render_walls(const SpecDev& S, const uint32_t* __
   // reports the step budget like the reference instead of spinning)
   const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h &&
                       (e.dx != 0.0 || e.dy != 0.0);
-  const int st = (S.sealed && inside && S.smem_map && S.n_doors < 32 && S.w >= 2)
+  const int st = (S.sealed && inside && S.w >= 2 &&
+                  ((S.smem_map && S.n_doors < 32) || (S.smem_u8 && S.n_doors <= 30)))
       ? wall_pass<NC, false, G, true>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo)
       : wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, zbuf_out, rayinfo,
                               S.sealed && inside);
@@ -2829,6 +2894,7 @@ struct tc_spec {
   size_t lean_smem = 0;
   int tab_bytes = 0;  // blob prefix holding the small tables
   int map_bytes = 0;  // blob prefix up to the end of the guarded stop codes
+  int code8_bytes = 0;  // blob prefix up to the end of the guarded u8 stop codes
 };
 
 namespace {
@@ -3077,7 +3143,8 @@ int launch_geometry(tc_spec* s) {
   if (d.npairs > 4) d.npairs = 4;
   d.warp_smem = warp_smem_layout(d, d.direct == 1 ? 0 : (d.mirror ? 2 * d.npairs : 2));
   d.smem_map = (d.h * d.w <= SMEM_MAP_MAX_CELLS) ? 1 : 0;
-  d.stage_bytes = d.smem_map ? s->map_bytes : s->tab_bytes;
+  d.smem_u8 = (!d.smem_map && s->code8_bytes <= SMEM_U8_MAX_BYTES) ? 1 : 0;
+  d.stage_bytes = d.smem_map ? s->map_bytes : (d.smem_u8 ? s->code8_bytes : s->tab_bytes);
   const size_t map_bytes = (size_t)map_smem_bytes(d);
   // + the per-CTA scratch of the step kernel (actions / rewards / dones)
   s->smem_bytes = map_bytes + (size_t)WARPS_PER_CTA * (32 / d.group) * d.warp_smem + CTA_SCRATCH;
@@ -3106,7 +3173,8 @@ int launch_geometry(tc_spec* s) {
   // lean kernel: a sealed map in shared memory, < 32 doors, the mirrored
   // lane-contiguous compose for full-warp groups (W / 16 divides 32, W <= 128)
   const char* ln = getenv("TILECAST_LEAN");
-  d.lean = (ln ? atoi(ln) != 0 : true) && d.sealed && d.smem_map && d.n_doors < 32 && d.w >= 2 &&
+  d.lean = (ln ? atoi(ln) != 0 : true) && d.sealed && d.w >= 2 &&
+           ((d.smem_map && d.n_doors < 32) || (d.smem_u8 && d.n_doors <= 30)) &&
            d.mirror && d.contig && d.direct == 1 && d.obs_w >= 32 && d.obs_w <= 128 &&
            32 % (d.obs_w / 16) == 0;
   if (d.lean) {
@@ -3239,6 +3307,16 @@ int tc_spec_create(const tc_tables* t, tc_spec** out) {
   const size_t o_ekind = b.add(t->ekind, t->n_entities);
   const size_t o_ecol = b.add(t->ecol, t->n_entities);
   const size_t tab_end = (b.bytes.size() + 15) & ~(size_t)15;
+  // u8 stop codes for large maps (0 floor, d + 1 door d, 31 wall), with the
+  // same w+1-cell wall guards as the u32 codes
+  std::vector<uint8_t> code8(cells.size() + 2 * (size_t)(t->w + 1), 31);
+  for (size_t k = 0; k < cells.size(); k++) {
+    const uint32_t tag = (cells[k] >> CELL_TAG_SHIFT) & 3u;
+    code8[(size_t)(t->w + 1) + k] =
+        tag == C_WALL ? 31 : tag == C_DOOR ? (uint8_t)((cells[k] & 31u) + 1) : 0;
+  }
+  const size_t o_code8 = b.add(code8.data(), code8.size()) + (size_t)(t->w + 1);
+  const size_t code8_end = (b.bytes.size() + 15) & ~(size_t)15;
   const size_t o_cell = b.add(cells.data(), cells.size() * 4);
   // stop codes with a wall guard of w+1 cells on each side (speculative DDA)
   std::vector<uint32_t> gsolid(solid.size() + 2 * (size_t)(t->w + 1), 0xffffffffu);
@@ -3275,7 +3353,9 @@ int tc_spec_create(const tc_tables* t, tc_spec** out) {
   d.b_goal = (int)o_goal; d.b_dcol = (int)o_dcol; d.b_dlock = (int)o_dlock;
   d.b_ekind = (int)o_ekind; d.b_ecol = (int)o_ecol; d.b_cell = (int)o_cell;
   d.b_solid = (int)o_solid;
+  d.b_code8 = (int)o_code8;
   s->tab_bytes = (int)tab_end;
+  s->code8_bytes = (int)code8_end;
   s->map_bytes = (int)map_end;
   for (int k = 0; k < FC_COUNT; k++) d.fc[k] = t->fc[k];
   for (int k = 0; k < 8; k++) d.dirs[k] = t->dirs[k];
