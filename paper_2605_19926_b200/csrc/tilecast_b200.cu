@@ -2325,13 +2325,18 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
 // MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387.
 // A group of G lanes owns one env at a time (G = 32: a warp; G = 16: each
 // half of a warp runs its own env).
-template <int NC, int G, int MINB, bool TAPS>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32, MINB)
-batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
-             const __grid_constant__ StateDev so, const long long* __restrict__ actions,
-             const __grid_constant__ OutDev out,
-             long long n, int mode, int auto_reset, int validate,
-             tc_counters* __restrict__ counters) {
+// The body is shared by batch_kernel (one spec, the whole grid) and
+// multi_kernel (one launch over several specs: each CTA belongs to one
+// group's contiguous CTA range); `cta` / `ncta` are the CTA's index within
+// its group's range and the range's size.
+template <int NC, int G, bool TAPS, bool FIX>
+__device__ __forceinline__ void batch_body(const SpecDev& S, const StateDev& st,
+                                           const StateDev& so,
+                                           const long long* __restrict__ actions,
+                                           const OutDev& out, long long n, int mode,
+                                           int auto_reset, int validate,
+                                           tc_counters* __restrict__ counters, int cta,
+                                           int ncta) {
   uint8_t* const smem = g_smem;
   constexpr int NG = 32 / G;  // groups per warp
   const Grp<G> g;
@@ -2363,16 +2368,16 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
   // zeroes it for the next launch).
   // Without counters (no ticket word) a multi-wave batch is interleaved
   // statically: env grp*grid + cta, then + stride.
-  const long long stride = (long long)gridDim.x * WARPS_PER_CTA * NG;
+  const long long stride = (long long)ncta * WARPS_PER_CTA * NG;
   const bool one_wave = n <= stride;
   const bool dyn = !one_wave && counters != nullptr;
-  const int epc = one_wave ? (int)((n + gridDim.x - 1) / gridDim.x) : 0;
-  const long long cbase = (long long)blockIdx.x * epc;
+  const int epc = one_wave ? (int)((n + ncta - 1) / ncta) : 0;
+  const long long cbase = (long long)cta * epc;
   const int cta_envs = one_wave ? (int)max(0LL, min((long long)epc, n - cbase)) : 0;
   // no env for this CTA; it still counts itself done on the mapped host path
-  if ((one_wave ? cta_envs == 0 : (long long)blockIdx.x >= n) && !out.res_host) return;
+  if ((one_wave ? cta_envs == 0 : (long long)cta >= n) && !out.res_host) return;
   const long long i_first = one_wave ? (grp < cta_envs ? cbase + grp : n)
-                                     : (long long)grp * gridDim.x + blockIdx.x;
+                                     : (long long)grp * ncta + cta;
   // per-CTA scratch after the group windows: actions / rewards / dones of
   // the CTA's envs (one-wave mapping)
   uint8_t* cta_s = smem + map_bytes + WARPS_PER_CTA * NG * S.warp_smem;
@@ -2463,7 +2468,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     if (status == TC_ST_OK) {
       // debug taps only in the TAPS instantiation (nullptr constants fold
       // the tap code out of the throughput kernel)
-      status = render_env<NC, G, (MINB <= 4)>(
+      status = render_env<NC, G, FIX>(
           S, cell, solid, sm, e, out.frames + (size_t)i * frame_bytes,
           (TAPS && out.zbuf) ? out.zbuf + (size_t)i * S.obs_w : nullptr,
           (TAPS && out.rayinfo) ? out.rayinfo + (size_t)i * S.obs_w * 4 : nullptr,
@@ -2510,7 +2515,7 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
     }
     if (threadIdx.x == 0) {
       __threadfence();
-      const bool last = atomicAdd(&counters->ctas_done, 1u) == gridDim.x - 1;
+      const bool last = atomicAdd(&counters->ctas_done, 1u) == (unsigned)ncta - 1;
       if (last) {
         counters->next_env = 0;
         counters->ctas_done = 0;
@@ -2564,6 +2569,138 @@ batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev
 // lean (7 CTAs of 4 warps per SM: a 4096-env batch is one wave). Envs whose
 // pose is off the grid or whose view direction is zero take the checked
 // wall pass out of line. _pycore.py:346-547 like batch_kernel.
+template <int NC, int G, int MINB, bool TAPS>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, MINB)
+batch_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
+             const __grid_constant__ StateDev so, const long long* __restrict__ actions,
+             const __grid_constant__ OutDev out,
+             long long n, int mode, int auto_reset, int validate,
+             tc_counters* __restrict__ counters) {
+  batch_body<NC, G, TAPS, (MINB <= 4)>(S, st, so, actions, out, n, mode, auto_reset, validate,
+                                       counters, blockIdx.x, gridDim.x);
+}
+
+// Heterogeneous-map step in ONE launch: up to TC_MULTI_MAX groups (spec g
+// over envs [off_g, off_g + n_g) of the batch, its own state blocks, output
+// views and counters). Work is handed out in blocks of one CTA pass (one env
+// per lane group) from ONE ticket counter, in group order: a CTA keeps its
+// staged spec while its tickets stay in the same group and restages (a new
+// TMA bulk copy, the group's launch record copied to shared memory) when it
+// crosses into the next group -- so the maps' different costs balance over
+// the whole grid instead of over fixed per-group CTA ranges. Lifts the
+// reference's homogeneous-batch limit.
+constexpr int TC_MULTI_MAX = 16;
+struct MultiGroup {
+  SpecDev spec;
+  StateDev st, so;
+  OutDev out;
+  long long n, off;
+  tc_counters* counters;
+};
+struct MultiArgs {
+  int n_groups;
+  long long total_blocks;
+  long long block_begin[TC_MULTI_MAX + 1];
+  tc_counters* ticket;  // the launch's block ticket / CTA count (group 0's counters)
+  MultiGroup g[TC_MULTI_MAX];
+};
+
+template <int NC, int G, int MINB>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, MINB)
+multi_kernel(const __grid_constant__ MultiArgs A, const long long* __restrict__ actions,
+             int auto_reset, int validate) {
+  constexpr int NG = 32 / G;
+  __shared__ __align__(16) MultiGroup s_grp;
+  __shared__ long long s_block;
+  uint8_t* const smem = g_smem;
+  const Grp<G> g;
+  const int lane = g.lane;
+  const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;
+  constexpr int PER_CTA = WARPS_PER_CTA * NG;
+  uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
+  const uint32_t *cell = nullptr, *solid = nullptr;
+  asm volatile("griddepcontrol.launch_dependents;");
+  int cur = -1;
+  bool waited = false;
+  const LaneGeo lg = lane_geo<G>(A.g[0].spec);
+  int bulk_pending = 0, buf = 0;
+  unsigned long long viol = 0;
+  uint32_t badbits = 0;
+  for (;;) {
+    if (waited) __syncthreads();  // the previous block is done with the staged spec
+    if (threadIdx.x == 0)
+      s_block = waited ? (long long)gridDim.x + atomicAdd(&A.ticket->next_env, 1u) : -1;
+    __syncthreads();
+    long long b = s_block;
+    if (!waited) {
+      // the first block is blockIdx.x (no ticket); stage before the wait
+      b = blockIdx.x;
+    }
+    if (b >= A.total_blocks) break;
+    int gi = 0;
+    while (gi + 1 < A.n_groups && b >= A.block_begin[gi + 1]) gi++;
+    if (gi != cur) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(&A.g[gi]);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(&s_grp);
+      for (int k = threadIdx.x; k < (int)(sizeof(MultiGroup) / 4); k += blockDim.x) dst[k] = src[k];
+      __syncthreads();
+      stage_map_issue(s_grp.spec, smap, cell, solid);
+      stage_map_wait();
+      cur = gi;
+    }
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+    }
+    const SpecDev& S = s_grp.spec;
+    const long long i = (b - A.block_begin[gi]) * PER_CTA + grp;
+    if (i < s_grp.n) {
+      const WarpSmem sm = carve(smem + map_smem_bytes(S) + grp * S.warp_smem);
+      const size_t frame_bytes = (size_t)S.obs_h * S.obs_w * 3;
+      const long long act = actions[s_grp.off + i];
+      Env e;
+      load_env<G>(S, s_grp.st, i, e);
+      int status = TC_ST_OK;
+      if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
+        status = TC_ST_BAD_ACTION;
+        store_env<G>(S, s_grp.so, i, e);
+      } else {
+        const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
+        if (lane == 0) {
+          s_grp.out.rewards[i] = o.reward;
+          s_grp.out.dones[i] = (uint8_t)o.done;
+          s_grp.out.truncs[i] = (uint8_t)o.trunc;
+          s_grp.out.events[i] = o.events;
+        }
+        viol += (unsigned long long)o.violation;
+        if (o.done && auto_reset) reset_draws(S, e);
+        store_env<G>(S, s_grp.so, i, e);
+        status = render_env<NC, G, (MINB <= 4)>(S, cell, solid, sm, e,
+                                                s_grp.out.frames + (size_t)i * frame_bytes,
+                                                nullptr, nullptr, nullptr, bulk_pending, buf,
+                                                lg, i);
+      }
+      if (lane == 0) s_grp.out.statuses[i] = status;
+      if (status != TC_ST_OK && lane == 0 && s_grp.counters)
+        atomicOr(&s_grp.counters->bad_status, 1u << status);
+      if (viol && lane == 0 && s_grp.counters) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_grp.counters->violations), viol);
+        viol = 0;
+      }
+    }
+  }
+  if (lane == 0 && bulk_pending) bulk_wait_all();
+  (void)badbits;
+  // the last CTA to finish re-arms the launch's ticket
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&A.ticket->ctas_done, 1u) == gridDim.x - 1) {
+      A.ticket->next_env = 0;
+      A.ticket->ctas_done = 0;
+    }
+  }
+}
+
 // Mapped host step, one wave: each warp parks its env's [reward | done] in
 // the CTA scratch right after the dynamics; at a CTA barrier warp 0 ships the
 // CTA's contiguous run to pinned host memory (one system fence per CTA) and
@@ -3489,6 +3626,94 @@ int tc_batch_step_into(const tc_spec* s, const tc_state* state_in, const tc_stat
                              auto_reset, validate, counters_dev, stream);
 }
 
+}  // extern "C"
+
+namespace {
+const void* select_multi(int nc, int group) {
+  if (group == 16) {
+    switch (nc) {
+      case 1: return (const void*)multi_kernel<1, 16, TC_MIN_CTAS16_WIDE>;
+      case 2: return (const void*)multi_kernel<2, 16, TC_MIN_CTAS16_WIDE>;
+      case 3: return (const void*)multi_kernel<3, 16, TC_MIN_CTAS16_WIDE>;
+      default: return (const void*)multi_kernel<4, 16, TC_MIN_CTAS16_WIDE>;
+    }
+  }
+  switch (nc) {
+    case 2: return (const void*)multi_kernel<2, 32, TC_MIN_CTAS>;
+    case 4: return (const void*)multi_kernel<4, 32, TC_MIN_CTAS>;
+    default: return nullptr;
+  }
+}
+
+// one multi_kernel launch: each group gets a contiguous CTA range sized by
+// its share of the envs (at least one CTA, at most one CTA per 8 / 4 envs),
+// out of one wave at the largest group's shared-memory footprint
+int launch_multi(const void* fn, const tc_spec* const* specs, const tc_state* states_in,
+                 const tc_state* states_out, const int64_t* actions_dev, const tc_out* outs,
+                 const int64_t* counts, int n_groups, int32_t auto_reset, int32_t validate,
+                 tc_counters* const* counters, void* stream) {
+  static thread_local MultiArgs A;
+  size_t smem = 0;
+  int64_t total = 0;
+  for (int g = 0; g < n_groups; g++) {
+    smem = std::max(smem, specs[g]->smem_bytes);
+    total += counts[g];
+  }
+  int dev = 0, optin = 0, per_sm = 0;
+  TC_CUDA(cudaGetDevice(&dev));
+  TC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  static thread_local const void* raised = nullptr;
+  if (raised != fn) {
+    TC_TRY_RC(raise_smem(fn, optin));
+    raised = fn;
+  }
+  TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS_PER_CTA * 32, smem));
+  if (per_sm < 1) return fail(TC_E_CAPACITY, "multi-map step does not fit on an SM");
+  const int wave = per_sm * device_sm_count();
+  const int per_cta = WARPS_PER_CTA * (32 / specs[0]->dev.group);
+  A.n_groups = n_groups;
+  A.block_begin[0] = 0;
+  A.ticket = counters[0];
+  int64_t off = 0;
+  for (int g = 0; g < n_groups; g++) {
+    A.block_begin[g + 1] = A.block_begin[g] + (counts[g] + per_cta - 1) / per_cta;
+    MultiGroup& m = A.g[g];
+    m.spec = specs[g]->dev;
+    m.st = to_dev(&states_in[g]);
+    m.so = to_dev(&states_out[g]);
+    m.out = to_dev(&outs[g]);
+    m.out.res_host = nullptr;
+    m.out.flag_host = nullptr;
+    m.n = counts[g];
+    m.off = off;
+    m.counters = counters[g];
+    off += counts[g];
+    if (specs[g]->dev.bulk && (reinterpret_cast<uintptr_t>(outs[g].frames) & 15u))
+      return fail(TC_E_INVALID, "frames must be 16-byte aligned");
+  }
+  A.total_blocks = A.block_begin[n_groups];
+  // block tickets start after the grid's first blocks (block = blockIdx.x)
+  const int grid = (int)std::min<int64_t>(wave, A.total_blocks);
+  const long long* acts = reinterpret_cast<const long long*>(actions_dev);
+  int ar = auto_reset, va = validate;
+  void* args[] = {&A, &acts, &ar, &va};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(WARPS_PER_CTA * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TC_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+  return TC_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int tc_multi_step(const tc_spec* const* specs, const tc_state* states_in,
                   const tc_state* states_out, const int64_t* actions_dev, const tc_out* outs,
                   const int64_t* counts, int32_t n_groups, int32_t auto_reset, int32_t validate,
@@ -3499,6 +3724,22 @@ int tc_multi_step(const tc_spec* const* specs, const tc_state* states_in,
   for (int g = 0; g < n_groups; g++) {
     if (!specs[g] || !counters[g]) return fail(TC_E_INVALID, "NULL spec / counters in a group");
     if (counts[g] < 1) return fail(TC_E_INVALID, "every group needs >= 1 env");
+  }
+  // ONE launch over all groups (multi_kernel) when they fit its group table
+  // and kernel set; TILECAST_MULTI_LAUNCH=0 selects the per-group launches
+  {
+    const char* ml = getenv("TILECAST_MULTI_LAUNCH");
+    const bool one = (ml ? atoi(ml) != 0 : true) && n_groups <= TC_MULTI_MAX && n_groups > 1;
+    const void* fn = one ? select_multi(specs[0]->nc, specs[0]->dev.group) : nullptr;
+    bool same = fn != nullptr;
+    for (int g = 1; g < n_groups && same; g++)
+      same = specs[g]->nc == specs[0]->nc && specs[g]->dev.group == specs[0]->dev.group &&
+             specs[g]->dev.obs_w == specs[0]->dev.obs_w &&
+             specs[g]->dev.obs_h == specs[0]->dev.obs_h;
+    if (same) {
+      return launch_multi(fn, specs, states_in, states_out, actions_dev, outs, counts, n_groups,
+                          auto_reset, validate, counters, stream);
+    }
   }
   // Groups run concurrently on side streams forked from / joined back into
   // the caller's stream, so one group's tail overlaps the others' work (each
