@@ -2741,16 +2741,20 @@ struct LeanSched {
   int ctas;  // one wave: CTAs that own envs (the mapped host step counts them)
 };
 
-template <int NC, bool ONE_WAVE, int FW, int FH>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32, TC_MIN_CTAS_LEAN)
+template <int NC, bool ONE_WAVE, int FW, int FH, int G, int MINB>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, MINB)
 lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
             const __grid_constant__ StateDev so, const long long* __restrict__ actions,
             const __grid_constant__ OutDev out, const __grid_constant__ LeanSched ls,
             int auto_reset, int validate, tc_counters* __restrict__ counters) {
-  constexpr int G = 32;
+  // G = 32: one env per warp (one-wave batches); G = 16: the two halves of
+  // a warp run one env each (multi-wave batches: the pair shares its
+  // convergent code, the issue-bound regime)
+  constexpr int NG = 32 / G, PER_CTA = WARPS_PER_CTA * NG;
+  const Grp<G> gr;
   uint8_t* const smem = g_smem;
-  const int lane = threadIdx.x & 31;
-  const int grp = threadIdx.x >> 5;
+  const int lane = gr.lane;
+  const int grp = (threadIdx.x >> 5) * NG + (threadIdx.x & 31) / G;
   uint32_t* smap = reinterpret_cast<uint32_t*>(smem);
   const uint32_t *cell, *solid;
 #if TC_TRACE
@@ -2784,8 +2788,8 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
 #endif
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
-  double* rew_s = reinterpret_cast<double*>(smem + map_bytes + WARPS_PER_CTA * S.warp_smem);
-  uint8_t* done_s = reinterpret_cast<uint8_t*>(rew_s + WARPS_PER_CTA);
+  double* rew_s = reinterpret_cast<double*>(smem + map_bytes + PER_CTA * S.warp_smem);
+  uint8_t* done_s = reinterpret_cast<uint8_t*>(rew_s + PER_CTA);
   // one wave, mapped: warps without an env still take part in the CTA's
   // result hand-off barrier
   if (ONE_WAVE && out.res_host && i >= n)
@@ -2857,7 +2861,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
         status = wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, nullptr, nullptr,
                                        false);
       }
-      __syncwarp();
+      gr.sync();
       TRACE(i, 3);
       if (status == TC_ST_OK) {
         const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
@@ -2882,7 +2886,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     }
 #endif
     if (ONE_WAVE) break;
-    i = counters ? __shfl_sync(0xffffffffu, tnext, 0) : i + ls.stride;
+    i = counters ? gr.shfl(tnext, 0) : i + ls.stride;
   }
 #if TC_TRACE
   if (g_trace_cta) {
@@ -3027,8 +3031,10 @@ struct tc_spec {
   int max_ctas = 0;    // grid size for one full wave
   int max_ctas_w = 0;  // the same for the multi-wave (wide) step kernel
   size_t smem_bytes = 0;
-  int lean_ctas = 0;   // grid size for one full wave of lean_kernel
+  int lean_ctas = 0;   // grid size for one full wave of lean_kernel (one env per warp)
   size_t lean_smem = 0;
+  int lean16_ctas = 0;  // the same for the two-envs-per-warp multi-wave lean kernel (0: none)
+  size_t lean16_smem = 0;
   int tab_bytes = 0;  // blob prefix holding the small tables
   int map_bytes = 0;  // blob prefix up to the end of the guarded stop codes
   int code8_bytes = 0;  // blob prefix up to the end of the guarded u8 stop codes
@@ -3133,19 +3139,33 @@ const void* select_rollout(int nc, int group) {
   }
 }
 
+#ifndef TC_MIN_CTAS_LEAN16
+#define TC_MIN_CTAS_LEAN16 5  // lean kernel, two envs per warp (multi-wave): 96 registers
+#endif
+// one-wave batches: one env per warp; multi-wave: two envs per warp (W <= 64)
 template <bool ONE_WAVE>
 const void* select_lean_t(int w, int h) {
-  if (w == 64 && h == 64) return (const void*)lean_kernel<2, ONE_WAVE, 64, 64>;
-  if (w == 128 && h == 128) return (const void*)lean_kernel<4, ONE_WAVE, 128, 128>;
+  if (!ONE_WAVE && w <= 64) {
+    if (w == 64 && h == 64) return (const void*)lean_kernel<4, false, 64, 64, 16, TC_MIN_CTAS_LEAN16>;
+    switch ((w + 15) / 16) {
+      case 2: return (const void*)lean_kernel<2, false, 0, 0, 16, TC_MIN_CTAS_LEAN16>;
+      default: return (const void*)lean_kernel<4, false, 0, 0, 16, TC_MIN_CTAS_LEAN16>;
+    }
+  }
+  if (w == 64 && h == 64) return (const void*)lean_kernel<2, ONE_WAVE, 64, 64, 32, TC_MIN_CTAS_LEAN>;
+  if (w == 128 && h == 128)
+    return (const void*)lean_kernel<4, ONE_WAVE, 128, 128, 32, TC_MIN_CTAS_LEAN>;
   switch (w / 32) {
-    case 1: return (const void*)lean_kernel<1, ONE_WAVE, 0, 0>;
-    case 2: return (const void*)lean_kernel<2, ONE_WAVE, 0, 0>;
-    default: return (const void*)lean_kernel<4, ONE_WAVE, 0, 0>;
+    case 1: return (const void*)lean_kernel<1, ONE_WAVE, 0, 0, 32, TC_MIN_CTAS_LEAN>;
+    case 2: return (const void*)lean_kernel<2, ONE_WAVE, 0, 0, 32, TC_MIN_CTAS_LEAN>;
+    default: return (const void*)lean_kernel<4, ONE_WAVE, 0, 0, 32, TC_MIN_CTAS_LEAN>;
   }
 }
 const void* select_lean(int w, int h, bool one_wave) {
   return one_wave ? select_lean_t<true>(w, h) : select_lean_t<false>(w, h);
 }
+// envs per CTA pass of the lean kernel
+int lean_per_cta(int w, bool one_wave) { return WARPS_PER_CTA * ((!one_wave && w <= 64) ? 2 : 1); }
 
 // validates host tables and builds the packed cell words
 int validate_tables(const tc_tables* t, std::vector<uint32_t>& cells,
@@ -3323,6 +3343,15 @@ int launch_geometry(tc_spec* s) {
                                                           s->lean_smem));
     if (per_sm < 1) d.lean = 0;
     s->lean_ctas = per_sm * device_sm_count();
+    s->lean16_ctas = 0;
+    const char* l16 = getenv("TILECAST_LEAN16");
+    if (d.lean && d.obs_w <= 64 && (l16 ? atoi(l16) != 0 : true)) {
+      const void* mf = select_lean(d.obs_w, d.obs_h, false);
+      s->lean16_smem = map_bytes + (size_t)WARPS_PER_CTA * 2 * d.warp_smem + CTA_SCRATCH;
+      TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mf, WARPS_PER_CTA * 32,
+                                                            s->lean16_smem));
+      s->lean16_ctas = per_sm * device_sm_count();
+    }
   }
   return TC_OK;
 }
@@ -3408,6 +3437,8 @@ const char* tc_step_kernel(const tc_spec* s, int64_t n) {
   const SpecDev& d = s->dev;
   if (d.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA)
     return "lean_kernel (one env per warp, one wave, 72 registers)";
+  if (d.lean && s->lean16_ctas > 0 && use_wide(s, n))
+    return "lean_kernel (two envs per warp, multi-wave env tickets, 96 registers)";
   if (use_wide(s, n))
     return d.group == 16 ? "batch_kernel (two envs per warp, multi-wave, 96 registers)"
                          : "batch_kernel (one env per warp, multi-wave)";
@@ -3551,15 +3582,18 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
   od.res_host = res_host;
   od.flag_host = flag_host;
   const bool taps = out->zbuf || out->rayinfo || out->spritevis;
-  // the lean one-env-per-warp kernel for batches that fit one wave of it
-  // (latency-bound: measured +15 % at 4096 envs); larger batches keep two
-  // envs per warp (issue-bound: the pair shares its convergent code,
-  // measured -6 % / -3 % for lean at 16384 / 8192 envs, -33 % at 131072)
-  const char* lw = getenv("TILECAST_LEAN_WAVES");
-  const int64_t lean_cap = (int64_t)s->lean_ctas * WARPS_PER_CTA * (lw ? atoi(lw) : 1);
-  if (mode == TC_MODE_STEP && !taps && d.lean && n <= lean_cap) {
-    const int64_t want = (n + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-    int grid = s->lean_ctas;
+  // the lean kernels: one env per warp for batches that fit one wave of it
+  // (latency-bound), two envs per warp over a full wave with env tickets for
+  // larger batches (issue-bound: the pair shares its convergent code)
+  const int64_t lean_cap = (int64_t)s->lean_ctas * WARPS_PER_CTA;
+  const bool lean1 = d.lean && n <= lean_cap;
+  // (a batch that still fits one wave of the two-envs-per-warp batch_kernel
+  // at 128 registers runs there: measured +7 % on the 160x128-tile map)
+  const bool lean2 = d.lean && !lean1 && s->lean16_ctas > 0 && use_wide(s, n);
+  if (mode == TC_MODE_STEP && !taps && (lean1 || lean2)) {
+    const int per_cta = lean1 ? WARPS_PER_CTA : 2 * WARPS_PER_CTA;
+    const int64_t want = (n + per_cta - 1) / per_cta;
+    int grid = lean1 ? s->lean_ctas : s->lean16_ctas;
     if (want < grid) {
       const int sms = device_sm_count();
       const int64_t g = (want + sms - 1) / sms * sms;
@@ -3567,8 +3601,8 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     }
     LeanSched ls;
     ls.n = n;
-    ls.stride = (long long)grid * WARPS_PER_CTA;
-    const bool one_wave = n <= ls.stride;
+    ls.stride = (long long)grid * per_cta;
+    const bool one_wave = lean1;
     ls.epc = one_wave ? (int)((n + grid - 1) / grid) : 0;
     ls.early = res_host != nullptr;
     ls.ctas = one_wave ? (int)((n + ls.epc - 1) / ls.epc) : 0;
@@ -3579,7 +3613,7 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(WARPS_PER_CTA * 32);
-    cfg.dynamicSmemBytes = s->lean_smem;
+    cfg.dynamicSmemBytes = lean1 ? s->lean_smem : s->lean16_smem;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
