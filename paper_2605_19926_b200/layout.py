@@ -2,8 +2,8 @@
 
 Values are part of the drop-in contract: they equal the reference's
 ``tilecast.backend.layout`` (/root/reference/pkg/src/tilecast/backend/layout.py:8-66)
-and the ``TC_*`` macros in ``include/tilecast_b200.h``; the CUDA library
-re-checks them at load time (``_native.check_layout``).
+and the ``TC_*`` macros in ``include/tilecast_b200.h``; ``_native`` asserts
+the status / mode / capacity constants against the library's at import.
 """
 
 # packed float constants, f64[FC_COUNT]  (layout.py:8-19)
