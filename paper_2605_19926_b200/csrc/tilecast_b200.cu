@@ -66,6 +66,9 @@ constexpr int WARPS_PER_CTA = 4;
 #ifndef TC_LOCKSTEP
 #define TC_LOCKSTEP 2  // rays per lane marched in lockstep on sealed maps
 #endif
+#ifndef TC_SPRITE_UNIFIED
+#define TC_SPRITE_UNIFIED 0  // 1 = one sprite pixel loop for the three kinds
+#endif
 #ifndef TC_STORE
 #define TC_STORE __stcs  // frame stores (direct path): streaming / evict-first
 #endif
@@ -1791,12 +1794,24 @@ __device__ __forceinline__ void mirror_direct(const SpecDev& S, const WarpSmem& 
 // the per-column and per-row terms in shared memory (_pycore.py:99-129
 // split into exact column and row factors: the same doubles and comparisons
 // as the reference), and the pixel written as one 16-bit + one 8-bit store.
-template <int KIND, int G>
+// One loop for the three kinds (instruction-cache footprint): with
+// e = ct + rt and x = cf & rf & 7 the reference's masks are
+//   goal   (e <= 0.8)                       -> colour 1
+//   key    (0.30 <= e <= 1.0) || x != 0     -> colour 1
+//   medkit (x & 3) -> colour 1, else (x & 4) -> colour 2
+// i.e. mk = (elo <= e <= ehi || (x & m1)) ? 1 : ((x & m2) ? 2 : 0) with
+// per-kind (elo, ehi, m1, m2); a medkit's terms are 0 and its e-range empty,
+// a goal's flags are 0.
+template <int G>
 __device__ __forceinline__ void sprite_pixels(uint8_t* __restrict__ frame, int row_bytes, int lo,
                                               int w, int r0, int h, const double* sct,
                                               const uint8_t* scf, const double* srt,
                                               const uint8_t* srf, uint32_t s1, uint32_t s2,
-                                              int lane) {
+                                              int kind, int lane) {
+  const double elo = kind == K_GOAL ? -dinf() : (kind == K_KEY ? 0.30 : dinf());
+  const double ehi = kind == K_GOAL ? 0.8 : 1.0;
+  const int m1 = kind == K_KEY ? 7 : (kind == K_MEDKIT ? 3 : 0);
+  const int m2 = kind == K_MEDKIT ? 4 : 0;
   const int npx = w * h;
   int pr = lane / w, pc = lane - (lane / w) * w;
   const int dr = G / w, dc = G - (G / w) * w;
@@ -1805,16 +1820,9 @@ __device__ __forceinline__ void sprite_pixels(uint8_t* __restrict__ frame, int r
     const int c = lo + pc, r = r0 + pr;
     const int cf = scf[c];
     if (cf & 0x80) {
-      int mk;
-      if (KIND == K_GOAL) {
-        mk = (sct[c] + srt[r] <= 0.8) ? 1 : 0;  // aa + |v-0.5|*2.0 <= 0.8
-      } else if (KIND == K_KEY) {
-        const double e = sct[c] + srt[r];      // ea*ea + ev*ev
-        mk = ((0.30 <= e && e <= 1.0) || (cf & srf[r] & 7) != 0) ? 1 : 0;
-      } else {
-        const int x = cf & srf[r] & 7;
-        mk = (x & 3) ? 1 : ((x & 4) ? 2 : 0);
-      }
+      const double e = sct[c] + srt[r];
+      const int x = cf & srf[r] & 7;
+      const int mk = ((elo <= e && e <= ehi) || (x & m1)) ? 1 : ((x & m2) ? 2 : 0);
       if (mk) {
         const uint32_t col = mk == 1 ? s1 : s2;
         uint8_t* d = frame + (size_t)r * row_bytes + c * 3;
@@ -1901,13 +1909,22 @@ __device__ __noinline__ void draw_sprites_direct(const SpecDev& S, WarpSmem sm, 
     }
     g.sync();
     const int w = hi - lo + 1, h = r.r1 - r.r0;
+#if TC_SPRITE_UNIFIED
+    sprite_pixels<G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2, r.kd,
+                     lane);
+#else
+    // one call site per kind: the kind is a constant inside each, so the
+    // unified loop's per-kind selects fold away
     if (r.kd == K_GOAL)
-      sprite_pixels<K_GOAL, G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2, lane);
+      sprite_pixels<G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2, K_GOAL,
+                       lane);
     else if (key)
-      sprite_pixels<K_KEY, G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2, lane);
+      sprite_pixels<G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2, K_KEY,
+                       lane);
     else
-      sprite_pixels<K_MEDKIT, G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2,
-                                 lane);
+      sprite_pixels<G>(frame, row_bytes, lo, w, r.r0, h, sct, scf, srt, srf, r.s1, r.s2,
+                       K_MEDKIT, lane);
+#endif
     g.sync();  // the next sprite reuses the term scratch; pixel order = draw order
   }
 }
@@ -1996,7 +2013,9 @@ __device__ __forceinline__ void mirror_contig_fixed(const SpecDev& S, const Warp
                  c2 = __byte_perm(C, 0, 0x2102);
   const uint32_t f0 = __byte_perm(F, 0, 0x0210), f1 = __byte_perm(F, 0, 0x1021),
                  f2 = __byte_perm(F, 0, 0x2102);
-#pragma unroll
+// (phases rolled: one copy of the row-pair code keeps the hot kernel small
+  // in the instruction cache when envs are in different phases at once)
+#pragma unroll 1
   for (int p = 0; p < 3; p++) {
     const int c = lane + G * p;
     const int rp = c / CPR, k = c - rp * CPR;
@@ -2739,6 +2758,9 @@ struct LeanSched {
   long long n, stride;
   int epc, early;
   int ctas;  // one wave: CTAs that own envs (the mapped host step counts them)
+  int stagger;  // one wave: 0 = all warps start together; k > 0 = the CTA's second
+                // half starts when its first half reached phase k (1 dynamics done,
+                // 2 walls done, 3 sprite setup done)
 };
 
 template <int NC, bool ONE_WAVE, int FW, int FH, int G, int MINB>
@@ -2778,6 +2800,8 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   // batch_kernel); device actions are read after griddepcontrol.wait
   long long act = 0;
   if (ls.early && i < n) act = actions[i];
+  __shared__ int s_go;
+  if (threadIdx.x == 0) s_go = 0;
   stage_map_issue(S, smap, cell, solid);
   stage_map_wait();
 #if TC_TRACE
@@ -2797,6 +2821,20 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   constexpr size_t FB = (size_t)FW * FH * 3;
   const size_t frame_bytes = FB ? FB : (size_t)S.obs_h * S.obs_w * 3;
   bool first = true;
+  // one-wave stagger: the CTA's first half of envs runs ahead so its frame
+  // writes overlap the second half's compute instead of every env of the
+  // grid reaching its compose at the same time
+  const int nfirst = (cta_envs + 1) >> 1;
+  const bool second = ONE_WAVE && ls.stagger && grp >= nfirst && i < n;
+  auto go_signal = [&](int phase) {
+    if (ONE_WAVE && ls.stagger == phase && grp < nfirst && lane == 0) atomicAdd(&s_go, 1);
+  };
+  if (second) {
+    if (lane == 0) {
+      while (*(volatile int*)&s_go < nfirst) __nanosleep(128);
+    }
+    gr.sync();
+  }
   while (i < n) {
     long long tnext = 0;
     if (!ONE_WAVE && lane == 0 && counters)
@@ -2824,6 +2862,9 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
       }
       if (ONE_WAVE && out.res_host)
         ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
+      go_signal(1);
+      go_signal(2);
+      go_signal(3);
     } else {
       TRACE(i, 1);
       const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
@@ -2846,6 +2887,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
         ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
       if (o.done && auto_reset) reset_draws(S, e);
       store_env<G>(S, so, i, e);
+      go_signal(1);
       TRACE(i, 2);
       uint8_t* frame = out.frames + (size_t)i * frame_bytes;
       const double planex = -e.dy * PLANE_HALF_WIDTH;
@@ -2862,18 +2904,23 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
                                        false);
       }
       gr.sync();
+      go_signal(2);
       TRACE(i, 3);
       if (status == TC_ST_OK) {
         const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
+        go_signal(3);
         TRACE(i, 4);
 #if TC_TRACE
         if (g_trace && lane == 0) g_trace[i * 16 + 7] = (unsigned long long)m;
 #endif
         if constexpr (FW != 0) mirror_contig_fixed<FW, FH, G>(S, sm, m, frame);
         else mirror_contig<NC, G>(S, sm, m, frame);
-      } else if (lane == 0) {
-        out.statuses[i] = status;
-        if (counters) atomicOr(&counters->bad_status, 1u << status);
+      } else {
+        go_signal(3);
+        if (lane == 0) {
+          out.statuses[i] = status;
+          if (counters) atomicOr(&counters->bad_status, 1u << status);
+        }
       }
     }
 #if TC_TRACE
@@ -3606,6 +3653,13 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     ls.epc = one_wave ? (int)((n + grid - 1) / grid) : 0;
     ls.early = res_host != nullptr;
     ls.ctas = one_wave ? (int)((n + ls.epc - 1) / ls.epc) : 0;
+    static const int stagger = [] {
+      const char* e = getenv("TILECAST_STAGGER");
+      return e ? atoi(e) : 0;
+    }();
+    // (not with the mapped host step: its CTA barrier after the dynamics
+    // needs every warp of the CTA)
+    ls.stagger = (one_wave && !res_host) ? stagger : 0;
     const long long* acts = reinterpret_cast<const long long*>(actions_dev);
     int ar = auto_reset, va = validate;
     SpecDev spec = d;
