@@ -263,6 +263,25 @@ __device__ __forceinline__ uint64_t draw_below(uint64_t key, unsigned long long&
   return __umul64hi(x, n);
 }
 
+// Exact small-integer <-> double conversions on the fp64 pipe instead of the
+// conversion unit: for 0 <= k < 2^31, double(k) = as_double(2^52 bits | k) -
+// 2^52; for 0 <= x < 2^52, floor(x) is the low word of x + 2^52 rounded
+// toward -inf (the ulp of 2^52 is 1).
+__device__ __forceinline__ double u2d_small(uint32_t k) {
+  return __longlong_as_double(0x4330000000000000LL | (long long)k) - 0x1p52;
+}
+__device__ __forceinline__ int floor_small(double x) {
+  return (int)(uint32_t)__double_as_longlong(__dadd_rd(x, 0x1p52));
+}
+// rgb_scale for shade in [0, 1] (every product in [0, 255]): the same
+// (int)(channel * shade) per channel, _pycore.py:168-170
+__device__ __forceinline__ uint32_t rgb_scale_unit(uint32_t rgb, double shade) {
+  const int r = floor_small(u2d_small(rgb & 0xffu) * shade);
+  const int g = floor_small(u2d_small((rgb >> 8) & 0xffu) * shade);
+  const int b = floor_small(u2d_small((rgb >> 16) & 0xffu) * shade);
+  return (uint32_t)(r & 0xff) | ((uint32_t)(g & 0xff) << 8) | ((uint32_t)(b & 0xff) << 16);
+}
+
 __device__ __forceinline__ uint32_t rgb_scale(uint32_t rgb, double shade) {
   // (int)(channel * shade) per channel, _pycore.py:168-170
   const int r = (int)((double)(rgb & 0xff) * shade);
@@ -684,9 +703,12 @@ __device__ __forceinline__ int line_half(int H, double perp) {
   const double e1 = fma(-perp, r1, 1.0);
   const double r2 = fma(r1, e1, r1);
   const double q = (double)H * r2;
-  const double fq = floor(q);
-  const double tol = q * 0x1p-40;
-  if (q < 999999999.0 && q - fq > tol && (fq + 1.0) - q > tol) return (int)fq / 2;
+  if (q < 999999999.0) {  // (false for NaN / inf too)
+    const int iq = floor_small(q);
+    const double fq = u2d_small((uint32_t)iq);
+    const double tol = q * 0x1p-40;
+    if (q - fq > tol && (fq + 1.0) - q > tol) return iq >> 1;
+  }
   double lh_f = (double)H / perp;
   if (lh_f > 1e9) lh_f = 1e9;
   return (int)lh_f / 2;
@@ -1226,7 +1248,7 @@ __device__ __forceinline__ int wall_pass(const SpecDev& S, const uint32_t* __res
 #pragma unroll
         for (int q = 0; q < LR; q++) {
           // shade = 1.0 / (1.0 + atten * perp) (IEEE reciprocal), _pycore.py:161-170
-          rgb[q] = rgb_scale(base[q], __drcp_rn(1.0 + atten * perp[q]));
+          rgb[q] = rgb_scale_unit(base[q], __drcp_rn(1.0 + atten * perp[q]));
           half[q] = line_half(H, perp[q]);
         }
 #pragma unroll
