@@ -28,6 +28,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include <algorithm>
 #include <mutex>
@@ -3112,6 +3113,12 @@ struct tc_spec {
 namespace {
 
 thread_local std::string g_err;
+thread_local double g_mapped_time[3] = {0.0, 0.0, 0.0};
+double host_us() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return 1e6 * (double)ts.tv_sec + 1e-3 * (double)ts.tv_nsec;
+}
 // programmatic dependent launch of consecutive steps (TILECAST_PDL=0 disables)
 const bool g_pdl = [] {
   const char* e = getenv("TILECAST_PDL");
@@ -3964,10 +3971,12 @@ int tc_batch_step_mapped(const tc_spec* s, const tc_state* state_in, const tc_st
   }
   volatile int32_t* done = flag_host + 1;
   *done = 0;
+  const double t0 = host_us();
   const int rc = launch_batch_kernel(s, state_in, state_out, actions_host, out, n, TC_MODE_STEP,
                                      auto_reset, validate, counters_dev, stream, results_host,
                                      flag_host);
   if (rc != TC_OK) return rc;
+  const double t1 = host_us();
   // the last CTA raises *done after the results reached host memory: spin
   // on it (the kernel's teardown and the stream's completion need not be
   // waited for); poll the stream now and then so a faulting kernel surfaces
@@ -3985,6 +3994,23 @@ int tc_batch_step_mapped(const tc_spec* s, const tc_state* state_in, const tc_st
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
+  const double t2 = host_us();
+  g_mapped_time[0] += t1 - t0;
+  g_mapped_time[1] += t2 - t1;
+  g_mapped_time[2] += 1.0;
+  return TC_OK;
+}
+
+// perf diagnostics of the mapped host step: mean host microseconds in the
+// launch call and in the wait for the completion word since the last reset
+int tc_debug_mapped_timing(double* out3, int32_t reset) {
+  if (out3) {
+    const double k = g_mapped_time[2] > 0 ? g_mapped_time[2] : 1.0;
+    out3[0] = g_mapped_time[0] / k;
+    out3[1] = g_mapped_time[1] / k;
+    out3[2] = g_mapped_time[2];
+  }
+  if (reset) g_mapped_time[0] = g_mapped_time[1] = g_mapped_time[2] = 0.0;
   return TC_OK;
 }
 
