@@ -144,6 +144,14 @@ const char *tc_build_info(void);
  * this spec launches (a description string; for reports). */
 const char *tc_step_kernel(const tc_spec *spec, int64_t n);
 
+/* Perf diagnostics (not part of the reference contract): per-env and
+ * per-CTA timestamp buffers (TC_TRACE builds only; TC_E_INVALID otherwise),
+ * and the mean host-side split of tc_batch_step_mapped (launch call, wait
+ * for the results, call count) since the last reset. */
+int tc_debug_trace(void *dev_buf);
+int tc_debug_trace_cta(void *dev_buf);
+int tc_debug_mapped_timing(double *out3, int32_t reset);
+
 /* Pack + upload a spec's tables once (replaces build_tables' device half,
  * tables.py:92-184). `host` points at host arrays. */
 int tc_spec_create(const tc_tables *host, tc_spec **out);
