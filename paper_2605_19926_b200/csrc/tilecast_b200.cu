@@ -3421,9 +3421,12 @@ int launch_geometry(tc_spec* s) {
     s->lean_ctas = per_sm * device_sm_count();
     s->lean16_ctas = 0;
     const char* l16 = getenv("TILECAST_LEAN16");
-    if (d.lean && d.obs_w <= 64 && (l16 ? atoi(l16) != 0 : true)) {
+    if (d.lean && (l16 ? atoi(l16) != 0 : true)) {
+      // multi-wave lean kernel: two envs per warp for W <= 64, one per warp
+      // (with tickets) for W = 128
       const void* mf = select_lean(d.obs_w, d.obs_h, false);
-      s->lean16_smem = map_bytes + (size_t)WARPS_PER_CTA * 2 * d.warp_smem + CTA_SCRATCH;
+      s->lean16_smem = map_bytes +
+                       (size_t)lean_per_cta(d.obs_w, false) * d.warp_smem + CTA_SCRATCH;
       TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mf, WARPS_PER_CTA * 32,
                                                             s->lean16_smem));
       s->lean16_ctas = per_sm * device_sm_count();
@@ -3514,7 +3517,8 @@ const char* tc_step_kernel(const tc_spec* s, int64_t n) {
   if (d.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA)
     return "lean_kernel (one env per warp, one wave, 72 registers)";
   if (d.lean && s->lean16_ctas > 0 && use_wide(s, n))
-    return "lean_kernel (two envs per warp, multi-wave env tickets, 96 registers)";
+    return d.obs_w <= 64 ? "lean_kernel (two envs per warp, multi-wave env tickets, 96 registers)"
+                         : "lean_kernel (one env per warp, multi-wave env tickets, 72 registers)";
   if (use_wide(s, n))
     return d.group == 16 ? "batch_kernel (two envs per warp, multi-wave, 96 registers)"
                          : "batch_kernel (one env per warp, multi-wave)";
@@ -3667,7 +3671,7 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
   // at 128 registers runs there: measured +7 % on the 160x128-tile map)
   const bool lean2 = d.lean && !lean1 && s->lean16_ctas > 0 && use_wide(s, n);
   if (mode == TC_MODE_STEP && !taps && (lean1 || lean2)) {
-    const int per_cta = lean1 ? WARPS_PER_CTA : 2 * WARPS_PER_CTA;
+    const int per_cta = lean_per_cta(d.obs_w, lean1);
     const int64_t want = (n + per_cta - 1) / per_cta;
     int grid = lean1 ? s->lean_ctas : s->lean16_ctas;
     if (want < grid) {
