@@ -627,29 +627,32 @@ __device__ __forceinline__ void bulk_wait_all() {
 //   recs: SpriteRec[E]
 //   band buffers: 2 x band_stride
 struct WarpSmem {
-  // one pointer per warp; the regions sit at host-computed offsets carried
-  // in SpecDev (constant-bank operands), so the compose / ray / sprite code
-  // does not keep a dozen 64-bit pointers live in registers
-  uint8_t* base;
-  __device__ __forceinline__ uint16_t* t0(const SpecDev& S) const { return (uint16_t*)(base + S.o_t0); }
-  __device__ __forceinline__ uint16_t* b0(const SpecDev& S) const { return (uint16_t*)(base + S.o_b0); }
-  __device__ __forceinline__ uint8_t* t8(const SpecDev& S) const { return base + S.o_t8; }
-  __device__ __forceinline__ uint32_t* wrgb(const SpecDev& S) const { return (uint32_t*)(base + S.o_wrgb); }
-  __device__ __forceinline__ uint8_t* wpk(const SpecDev& S) const { return base + S.o_wpk; }
-  __device__ __forceinline__ uint8_t* tpk(const SpecDev& S) const { return base + S.o_tpk; }
-  __device__ __forceinline__ double* sct(const SpecDev& S) const { return (double*)(base + S.o_sct); }
+  // one 32-bit offset into the dynamic shared memory per lane group; the
+  // regions sit at host-computed offsets carried in SpecDev (constant-bank
+  // operands), so the compose / ray / sprite code does not keep a dozen
+  // 64-bit pointers live in registers, and every access -- also inside the
+  // out-of-line functions that receive a WarpSmem -- is visibly a
+  // shared-memory access (LDS / STS, not a generic load)
+  uint32_t off;
+  __device__ __forceinline__ uint16_t* t0(const SpecDev& S) const { return (uint16_t*)(g_smem + off + S.o_t0); }
+  __device__ __forceinline__ uint16_t* b0(const SpecDev& S) const { return (uint16_t*)(g_smem + off + S.o_b0); }
+  __device__ __forceinline__ uint8_t* t8(const SpecDev& S) const { return g_smem + off + S.o_t8; }
+  __device__ __forceinline__ uint32_t* wrgb(const SpecDev& S) const { return (uint32_t*)(g_smem + off + S.o_wrgb); }
+  __device__ __forceinline__ uint8_t* wpk(const SpecDev& S) const { return g_smem + off + S.o_wpk; }
+  __device__ __forceinline__ uint8_t* tpk(const SpecDev& S) const { return g_smem + off + S.o_tpk; }
+  __device__ __forceinline__ double* sct(const SpecDev& S) const { return (double*)(g_smem + off + S.o_sct); }
   __device__ __forceinline__ uint8_t* scf(const SpecDev& S) const {
-    return base + S.o_sct + 8 * ((S.obs_w + 15) & ~15);
+    return g_smem + off + S.o_sct + 8 * ((S.obs_w + 15) & ~15);
   }
-  __device__ __forceinline__ double* srt(const SpecDev& S) const { return (double*)(base + S.o_srow); }
+  __device__ __forceinline__ double* srt(const SpecDev& S) const { return (double*)(g_smem + off + S.o_srow); }
   __device__ __forceinline__ uint8_t* srf(const SpecDev& S) const {
-    return base + S.o_srow + 8 * ((S.obs_h + 15) & ~15);
+    return g_smem + off + S.o_srow + 8 * ((S.obs_h + 15) & ~15);
   }
-  __device__ __forceinline__ double* zbuf(const SpecDev& S) const { return (double*)(base + S.o_zbuf); }
-  __device__ __forceinline__ double* gdep(const SpecDev& S) const { return (double*)(base + S.o_gdep); }
-  __device__ __forceinline__ SpriteRec* recs(const SpecDev& S) const { return (SpriteRec*)(base + S.o_recs); }
+  __device__ __forceinline__ double* zbuf(const SpecDev& S) const { return (double*)(g_smem + off + S.o_zbuf); }
+  __device__ __forceinline__ double* gdep(const SpecDev& S) const { return (double*)(g_smem + off + S.o_gdep); }
+  __device__ __forceinline__ SpriteRec* recs(const SpecDev& S) const { return (SpriteRec*)(g_smem + off + S.o_recs); }
   __device__ __forceinline__ uint8_t* band(const SpecDev& S, int k) const {
-    return base + S.o_band + k * S.band_stride;
+    return g_smem + off + S.o_band + k * S.band_stride;
   }
 };
 
@@ -685,7 +688,7 @@ __host__ inline int warp_smem_layout(SpecDev& d, int nbands) {
 
 __device__ inline WarpSmem carve(uint8_t* base) {
   WarpSmem m;
-  m.base = base;
+  m.off = (uint32_t)(base - g_smem);
   return m;
 }
 
@@ -1847,11 +1850,14 @@ __device__ __forceinline__ void sprite_pixels(uint8_t* __restrict__ frame, int r
       const int x = cf & srf[r] & 7;
       const int mk = ((elo <= e && e <= ehi) || (x & m1)) ? 1 : ((x & m2) ? 2 : 0);
       if (mk) {
+        // three byte stores at immediate offsets from one global address
         const uint32_t col = mk == 1 ? s1 : s2;
-        uint8_t* d = frame + (size_t)r * row_bytes + c * 3;
-        const int odd = (int)(reinterpret_cast<uintptr_t>(d) & 1u);
-        *reinterpret_cast<uint16_t*>(d + odd) = (uint16_t)(col >> (8 * odd));
-        d[odd ? 0 : 2] = (uint8_t)(odd ? col : col >> 16);
+        uint8_t* d = frame + (uint32_t)(r * row_bytes + c * 3);  // < 2^31 per frame
+        asm volatile(
+            "st.global.u8 [%0], %1;\n\t"
+            "st.global.u8 [%0+1], %2;\n\t"
+            "st.global.u8 [%0+2], %3;"
+            ::"l"(d), "r"(col), "r"(col >> 8), "r"(col >> 16) : "memory");
       }
     }
     pc += dc;
