@@ -397,16 +397,27 @@ def main():
         launch_batch(bs._ds, bs._sb, acts[s], outs[s % ring], n, L.MODE_STEP, True, False,
                      bs._counters)
 
+    # value: K steps through tc.batch_steps -- K launches of the step kernel,
+    # each writing its own output block of the ring, chained per CTA (a
+    # step's CTAs start as the previous step's CTAs free their slots; each
+    # env waits only for its own state) -- captured once into a CUDA graph
+    # (launch-bound at 4096 envs otherwise); replaying it runs exactly K steps
+    bsc = [tc.batch_reset(spec, n, seed, device=dev, base=base, n_total=n_total)]
+    bsc[0] = tc.batch_steps(bsc[0], acts[:args.warmup], outs=outs)
     for s in range(args.warmup):
         step(s)
     torch.cuda.synchronize(dev)
-    # the K timed launches are captured once into a CUDA graph (launch-bound
-    # at 4096 envs otherwise); replaying it runs exactly K fused steps
     graph = torch.cuda.CUDAGraph()
     cap = torch.cuda.Stream(dev)
     cap.wait_stream(stream)
     with torch.cuda.stream(cap):
         with torch.cuda.graph(graph, stream=cap):
+            bsc[0] = tc.batch_steps(bsc[0], acts[args.warmup:args.warmup + args.steps], outs=outs)
+    # the same K steps as K unchained launches (each waits for the whole
+    # previous grid), reported beside it
+    graph_u = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(graph_u, stream=cap):
             for k in range(args.steps):
                 step(args.warmup + k)
     torch.cuda.synchronize(dev)
@@ -428,13 +439,25 @@ def main():
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
+        u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clock_warm(stream)
+        u0.record(stream)
+        graph_u.replay()
+        u1.record(stream)
+        torch.cuda.synchronize(dev)
     elapsed_ms = t_start.elapsed_time(t_end)
+    unchained_ms = u0.elapsed_time(u1)
+    if world > 1:
+        t = torch.tensor([unchained_ms], dtype=torch.float64, device=rdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        unchained_ms = float(t.item())
     kern_ms = [elapsed_ms / args.steps]  # per-launch average over the graph replay
     if world > 1:
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
     bs.check()
+    bsc[0].check()
     value = n_total * args.steps / (elapsed_ms / 1e3)
 
     # fused multi-step launch (tc_rollout: K steps, in-kernel policy) for context
@@ -535,6 +558,11 @@ def main():
                          # best of 5; ~7.4 TB/s on B200, above the copy figure)
                          "write_peak_gbs": write_peak,
                          "frac_of_write_peak": achieved / write_peak if write_peak else None},
+            "api": "tc.batch_steps (K step launches chained per CTA, tc_batch_steps)",
+            "unchained": {"value": n_total * args.steps / (unchained_ms / 1e3),
+                          "unit": "env-steps/s", "ms_per_step": unchained_ms / args.steps,
+                          "api": "K tc_batch_kernel launches, each after the whole previous "
+                                 "grid (griddepcontrol.wait)"},
             "rollout_fused": {"value": rollout_value, "unit": "env-steps/s",
                               "launches": 1, "steps_per_launch": args.steps},
             "gpu_launches": args.steps,

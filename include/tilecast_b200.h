@@ -177,14 +177,32 @@ int tc_batch_step_into(const tc_spec *spec, const tc_state *state_in,
                        const tc_out *out, int64_t n, int32_t auto_reset,
                        int32_t validate, tc_counters *counters_dev, void *stream);
 
+/* K consecutive steps (K x batch_step, batch.py:109-138, auto-reset) as K
+ * launches of the lean one-wave kernel with CTA-granular chaining instead of
+ * a grid-wide wait between them: state ping-pongs a -> b -> a ..., step k
+ * reads actions_dev[k * n .. k * n + n) and writes outs[k % ring]; the final
+ * state is in b when k_steps is odd, else in a. flags_dev: device u32[2 * n]
+ * zeroed once per batch; epoch0: a per-batch counter the caller advances by
+ * k_steps per call (epochs are never reused). Env i of step k waits only for
+ * its own state from step k - 1 (and for the step that last wrote
+ * outs[k % ring]); the first step waits for all prior work on the stream, so
+ * the action table may come from any earlier kernel. Batches that do not fit
+ * one wave of the lean kernel get K ordinary launches. */
+int tc_batch_steps(const tc_spec *spec, const tc_state *state_a,
+                   const tc_state *state_b, const int64_t *actions_dev,
+                   const tc_out *outs, int32_t ring, int64_t n, int32_t k_steps,
+                   int32_t auto_reset, int32_t validate,
+                   tc_counters *counters_dev, uint32_t *flags_dev,
+                   uint32_t epoch0, void *stream);
+
 /* Heterogeneous-map step (the reference steps one
  * homogeneous batch per batch_kernel call, tables.py:251-273):
  * n_groups out-of-place steps, group g = counts[g] envs of specs[g] with
  * states_in[g] -> states_out[g], actions actions_dev[offset_g ..], outputs
  * outs[g] (typically views of one batch-wide block), counters[g] (one per
- * group). The groups run concurrently on library-owned side streams forked
- * from and joined back into `stream`; the call is asynchronous like
- * tc_batch_step_into. */
+ * group), in ONE launch (up to 16 groups with a common frame shape; more
+ * groups run as concurrent launches on library-owned side streams forked
+ * from and joined back into `stream`); asynchronous like tc_batch_step_into. */
 int tc_multi_step(const tc_spec *const *specs, const tc_state *states_in,
                   const tc_state *states_out, const int64_t *actions_dev,
                   const tc_out *outs, const int64_t *counts, int32_t n_groups,

@@ -89,6 +89,8 @@ def _load() -> C.CDLL:
                                       C.c_int32, C.c_int32, _p, _p]),
         "tc_batch_step_into": (C.c_int, [_p, P(TcState), P(TcState), _p, P(TcOut), C.c_int64,
                                          C.c_int32, C.c_int32, _p, _p]),
+        "tc_batch_steps": (C.c_int, [_p, P(TcState), P(TcState), _p, _p, C.c_int32, C.c_int64,
+                                     C.c_int32, C.c_int32, C.c_int32, _p, _p, C.c_uint32, _p]),
         "tc_multi_step": (C.c_int, [_p, P(TcState), P(TcState), _p, P(TcOut), _p, C.c_int32,
                                     C.c_int32, C.c_int32, _p, _p]),
         "tc_batch_step_host": (C.c_int, [_p, P(TcState), P(TcState), _p, _p, P(TcOut), C.c_int64,

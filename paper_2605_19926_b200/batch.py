@@ -59,6 +59,10 @@ class BatchState:
     n_total: int = 0
     _retired: tuple = field(default=(), repr=False)
     _stage: "_ActionStage | None" = field(default=None, repr=False)
+    # chained multi-step launches (batch_steps): per-env / per-CTA epoch
+    # flags in device memory and the batch's next epoch (one list shared by
+    # the whole lineage of states)
+    _chain: list = field(default_factory=list, repr=False)
 
     @property
     def device(self) -> torch.device:
@@ -173,6 +177,55 @@ def batch_reset(spec: EnvSpec, n: int, seed: int, *, device=None, base: int = 0,
                       base=base, n_total=n_total if n_total is not None else base + n)
 
 
+def batch_steps(bs: BatchState, actions: torch.Tensor, *, outs: Sequence[DeviceOut] | None = None,
+                validate: bool = False) -> BatchState:
+    """K consecutive batch_steps (auto-reset) in one native call:
+    ``actions`` is a (K, n) int64 CUDA tensor, row k = step k's actions.
+    K launches of the step kernel chained at CTA granularity
+    (tc_batch_steps: a step's CTAs start as the previous step's CTAs free
+    their slots, each env waiting only for its own state), equal to K
+    ``batch_step`` calls with ``reuse=True``. ``outs`` is a ring of output
+    blocks (step k writes ``outs[k % len(outs)]``; default: a second block,
+    then this batch's own block, as ``reuse=True`` recycles it).
+    Returns the state after the last step, whose ``frames`` / ``_ob`` are
+    that step's output block. The states between are not returned (the two
+    state blocks ping-pong)."""
+    t = bs.spec.tables
+    if not (isinstance(actions, torch.Tensor) and actions.is_cuda and actions.dim() == 2
+            and actions.shape[1] == bs.n):
+        raise ContractError(f"actions must be a (K, {bs.n}) CUDA tensor")
+    acts = actions.to(torch.int64).contiguous()
+    k = acts.shape[0]
+    if k == 0:
+        return bs
+    if outs is None:
+        other = bs._retired[1] if bs._retired else DeviceOut.alloc(
+            bs.n, t.obs_height, t.obs_width, bs.device)
+        outs = [other, bs._ob] if k > 1 else [other]  # bs's own block is recycled from step 1
+    outs = list(outs)
+    sb = bs._retired[0] if bs._retired else DeviceState.alloc(bs.n, t.n_doors, t.n_entities,
+                                                               bs.device)
+    if not bs._chain:
+        bs._chain.extend([torch.zeros(2 * bs.n, dtype=torch.int32, device=bs.device), 1])
+    flags, epoch = bs._chain
+    ring = (N.TcOut * len(outs))(*[o.c_struct() for o in outs])
+    with torch.cuda.device(bs.device):
+        N.check(N.lib().tc_batch_steps(
+            bs._ds.handle, N.C.byref(bs._sb.c_struct()), N.C.byref(sb.c_struct()), N.ptr(acts),
+            ring, len(outs), bs.n, k, 1, 1 if validate else 0, N.ptr(bs._counters),
+            N.ptr(flags), epoch & 0xFFFFFFFF, stream_ptr(bs.device)), "tc_batch_steps")
+    bs._chain[1] = epoch + k
+    final_sb, spare_sb = (sb, bs._sb) if k % 2 == 1 else (bs._sb, sb)
+    final_ob = outs[(k - 1) % len(outs)]
+    spare_ob = outs[(k - 2) % len(outs)] if len(outs) > 1 else bs._ob
+    new = BatchState(spec=bs.spec, n=bs.n, _ds=bs._ds, _sb=final_sb, _ob=final_ob,
+                     _counters=bs._counters, base=bs.base, n_total=bs.n_total,
+                     _retired=(spare_sb, spare_ob), _stage=bs._stage, _chain=bs._chain)
+    if validate:
+        new.check()
+    return new
+
+
 def _coerce_actions(bs: BatchState, actions) -> torch.Tensor:
     """Host-side contract checks (batch.py:92-106), then an async H2D copy
     through a pinned staging buffer. CUDA tensors are checked on the device."""
@@ -283,7 +336,8 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
     dones = stg.h_done.copy()
     new = BatchState(spec=spec, n=bs.n, _ds=bs._ds, _sb=sb, _ob=ob, _counters=bs._counters,
                      base=bs.base, n_total=bs.n_total,
-                     _retired=(bs._sb, bs._ob) if reuse else (), _stage=bs._stage)
+                     _retired=(bs._sb, bs._ob) if reuse else (), _stage=bs._stage,
+                     _chain=bs._chain)
     if validate:
         new.check()
     return new, rewards, dones
@@ -313,7 +367,7 @@ def batch_step(bs: BatchState, actions: Sequence[Action | int] | np.ndarray | to
     new = BatchState(spec=spec, n=bs.n, _ds=bs._ds, _sb=sb, _ob=ob, _counters=bs._counters,
                      base=bs.base, n_total=bs.n_total,
                      _retired=(bs._sb, bs._ob) if reuse else (),
-                     _stage=bs._stage)
+                     _stage=bs._stage, _chain=bs._chain)
     if validate or sync_checks:
         new.check()
     rewards, dones = ob.rewards, ob.dones.view(torch.bool)

@@ -2787,10 +2787,26 @@ struct LeanSched {
   long long n, stride;
   int epc, early;
   int ctas;  // one wave: CTAs that own envs (the mapped host step counts them)
-  int stagger;  // one wave: 0 = all warps start together; k > 0 = the CTA's second
-                // half starts when its first half reached phase k (1 dynamics done,
-                // 2 walls done, 3 sprite setup done)
+  // Chained steps (tc_batch_steps, one wave): per-env "state written" and
+  // per-CTA "frames written" epochs in device memory (flags = [ready u32[n] |
+  // done u32[ctas]]). A launch with need_ready != 0 skips the grid-wide
+  // griddepcontrol.wait: env i waits only for ready[i] >= need_ready (its
+  // state from the previous step) and, when need_done != 0, for the CTA's
+  // done[] >= need_done (the output block it is about to overwrite was
+  // finished), so a step's CTAs start as soon as the previous step's CTAs
+  // free their slots instead of after its slowest CTA.
+  unsigned int* flags;
+  unsigned int epoch, need_ready, need_done;
 };
+
+// chained steps: env i's state is in memory -- every lane fences its own
+// stores (store_env spreads them over lanes), then lane 0 publishes the epoch
+template <class Grp_>
+__device__ __forceinline__ void state_ready(const Grp_& g, const LeanSched& ls, long long i) {
+  __threadfence();
+  g.sync();
+  if (g.lane == 0) *(volatile unsigned int*)(ls.flags + i) = ls.epoch;
+}
 
 template <int NC, bool ONE_WAVE, int FW, int FH, int G, int MINB>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, MINB)
@@ -2829,14 +2845,13 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   // batch_kernel); device actions are read after griddepcontrol.wait
   long long act = 0;
   if (ls.early && i < n) act = actions[i];
-  __shared__ int s_go;
-  if (threadIdx.x == 0) s_go = 0;
   stage_map_issue(S, smap, cell, solid);
   stage_map_wait();
 #if TC_TRACE
   if (g_trace_cta && threadIdx.x == 0) tcta[1] = gtime();
 #endif
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const bool chained = ONE_WAVE && ls.flags != nullptr && ls.need_ready != 0;
+  if (!chained) asm volatile("griddepcontrol.wait;" ::: "memory");
 #if TC_TRACE
   if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
 #endif
@@ -2850,19 +2865,18 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   constexpr size_t FB = (size_t)FW * FH * 3;
   const size_t frame_bytes = FB ? FB : (size_t)S.obs_h * S.obs_w * 3;
   bool first = true;
-  // one-wave stagger: the CTA's first half of envs runs ahead so its frame
-  // writes overlap the second half's compute instead of every env of the
-  // grid reaching its compose at the same time
-  const int nfirst = (cta_envs + 1) >> 1;
-  const bool second = ONE_WAVE && ls.stagger && grp >= nfirst && i < n;
-  auto go_signal = [&](int phase) {
-    if (ONE_WAVE && ls.stagger == phase && grp < nfirst && lane == 0) atomicAdd(&s_go, 1);
-  };
-  if (second) {
+  if (chained && i < n) {
+    // this env's state from the previous step, and (need_done) the output
+    // block this launch overwrites finished by the step that last wrote it
     if (lane == 0) {
-      while (*(volatile int*)&s_go < nfirst) __nanosleep(128);
+      const volatile unsigned int* rd = ls.flags + i;
+      const volatile unsigned int* dn = ls.flags + n + blockIdx.x;
+      while ((int)(*rd - ls.need_ready) < 0 ||
+             (ls.need_done != 0 && (int)(*dn - ls.need_done) < 0))
+        __nanosleep(64);
     }
     gr.sync();
+    __threadfence();  // acquire: the flag's writer fenced before setting it
   }
   while (i < n) {
     long long tnext = 0;
@@ -2877,6 +2891,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     // known, so nothing but the env index stays live across the render
     if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
       store_env<G>(S, so, i, e);  // out-of-place: carry the state over
+      if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
       if (lane == 0) {
         out.statuses[i] = TC_ST_BAD_ACTION;
         if (out.flag_host) {
@@ -2891,9 +2906,6 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
       }
       if (ONE_WAVE && out.res_host)
         ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
-      go_signal(1);
-      go_signal(2);
-      go_signal(3);
     } else {
       TRACE(i, 1);
       const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
@@ -2916,7 +2928,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
         ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
       if (o.done && auto_reset) reset_draws(S, e);
       store_env<G>(S, so, i, e);
-      go_signal(1);
+      if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
       TRACE(i, 2);
       uint8_t* frame = out.frames + (size_t)i * frame_bytes;
       const double planex = -e.dy * PLANE_HALF_WIDTH;
@@ -2933,23 +2945,18 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
                                        false);
       }
       gr.sync();
-      go_signal(2);
       TRACE(i, 3);
       if (status == TC_ST_OK) {
         const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
-        go_signal(3);
         TRACE(i, 4);
 #if TC_TRACE
         if (g_trace && lane == 0) g_trace[i * 16 + 7] = (unsigned long long)m;
 #endif
         if constexpr (FW != 0) mirror_contig_fixed<FW, FH, G>(S, sm, m, frame);
         else mirror_contig<NC, G>(S, sm, m, frame);
-      } else {
-        go_signal(3);
-        if (lane == 0) {
-          out.statuses[i] = status;
-          if (counters) atomicOr(&counters->bad_status, 1u << status);
-        }
+      } else if (lane == 0) {
+        out.statuses[i] = status;
+        if (counters) atomicOr(&counters->bad_status, 1u << status);
       }
     }
 #if TC_TRACE
@@ -2974,8 +2981,14 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     }
   }
 #endif
-  // one wave: the host was released by results_done as soon as every env's
-  // reward / done had reached it; nothing left to count
+  if (ONE_WAVE && ls.flags) {
+    // every warp's frame writes are performed before the CTA's done epoch
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *(volatile unsigned int*)(ls.flags + n + blockIdx.x) = ls.epoch;
+  }
+  // one wave: the mapped host step was released by ship_results as soon as
+  // every env's reward / done had reached the host; nothing left to count
   if (ONE_WAVE || !counters) return;
   {
     volatile int& s_last = *reinterpret_cast<int*>(smem);
@@ -3645,11 +3658,17 @@ int tc_spec_destroy(tc_spec* s) {
   return e == cudaSuccess ? TC_OK : cuda_fail(e, "cudaFree(spec)");
 }
 
+struct ChainArgs {
+  unsigned int* flags;
+  unsigned int epoch, need_ready, need_done;
+};
+
 static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc_state* state_out,
                                const int64_t* actions_dev, const tc_out* out, int64_t n,
                                int32_t mode, int32_t auto_reset, int32_t validate,
                                tc_counters* counters_dev, void* stream,
-                               uint8_t* res_host = nullptr, int32_t* flag_host = nullptr) {
+                               uint8_t* res_host = nullptr, int32_t* flag_host = nullptr,
+                               const ChainArgs* chain = nullptr) {
   if (!s || !state || !out) return fail(TC_E_INVALID, "NULL spec/state/out");
   if (n < 0) return fail(TC_E_INVALID, "n must be >= 0");
   if (mode != TC_MODE_RESET && mode != TC_MODE_STEP && mode != MODE_RENDER)
@@ -3692,13 +3711,14 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     ls.epc = one_wave ? (int)((n + grid - 1) / grid) : 0;
     ls.early = res_host != nullptr;
     ls.ctas = one_wave ? (int)((n + ls.epc - 1) / ls.epc) : 0;
-    static const int stagger = [] {
-      const char* e = getenv("TILECAST_STAGGER");
-      return e ? atoi(e) : 0;
-    }();
-    // (not with the mapped host step: its CTA barrier after the dynamics
-    // needs every warp of the CTA)
-    ls.stagger = (one_wave && !res_host) ? stagger : 0;
+    ls.flags = nullptr;
+    ls.epoch = ls.need_ready = ls.need_done = 0;
+    if (chain && one_wave && !res_host) {
+      ls.flags = chain->flags;
+      ls.epoch = chain->epoch;
+      ls.need_ready = chain->need_ready;
+      ls.need_done = chain->need_done;
+    }
     const long long* acts = reinterpret_cast<const long long*>(actions_dev);
     int ar = auto_reset, va = validate;
     SpecDev spec = d;
@@ -3742,6 +3762,38 @@ int tc_batch_kernel(const tc_spec* s, const tc_state* state, const int64_t* acti
                     int32_t validate, tc_counters* counters_dev, void* stream) {
   return launch_batch_kernel(s, state, nullptr, actions_dev, out, n, mode, auto_reset, validate,
                              counters_dev, stream);
+}
+
+int tc_batch_steps(const tc_spec* s, const tc_state* state_a, const tc_state* state_b,
+                   const int64_t* actions_dev, const tc_out* outs, int32_t ring, int64_t n,
+                   int32_t k_steps, int32_t auto_reset, int32_t validate,
+                   tc_counters* counters_dev, uint32_t* flags_dev, uint32_t epoch0,
+                   void* stream) {
+  if (!state_a || !state_b || !actions_dev || !outs || !flags_dev)
+    return fail(TC_E_INVALID, "NULL state / actions / outs / flags");
+  if (ring < 1 || k_steps < 0 || n < 0) return fail(TC_E_INVALID, "bad ring / k / n");
+  if (k_steps == 0 || n == 0) return TC_OK;
+  // chaining needs the lean one-wave kernel (its fixed CTA -> env mapping);
+  // other batches get K ordinary launches
+  const bool chain_ok = s && s->dev.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA;
+  for (int k = 0; k < k_steps; k++) {
+    const tc_state* in = (k & 1) ? state_b : state_a;
+    const tc_state* outst = (k & 1) ? state_a : state_b;
+    ChainArgs ca;
+    ca.flags = flags_dev;
+    ca.epoch = epoch0 + (uint32_t)k;
+    // the first launch waits for the whole previous grid (whatever it was);
+    // each later one for its env's state from step k - 1 and, once the ring
+    // wraps, for the step that last wrote the output block it overwrites
+    ca.need_ready = k == 0 ? 0u : ca.epoch - 1u;
+    ca.need_done = (k >= ring) ? ca.epoch - (uint32_t)ring : 0u;
+    const int rc = launch_batch_kernel(s, in, outst, actions_dev + (size_t)k * (size_t)n,
+                                       &outs[k % ring], n, TC_MODE_STEP, auto_reset, validate,
+                                       counters_dev, stream, nullptr, nullptr,
+                                       chain_ok ? &ca : nullptr);
+    if (rc != TC_OK) return rc;
+  }
+  return TC_OK;
 }
 
 int tc_batch_step_into(const tc_spec* s, const tc_state* state_in, const tc_state* state_out,

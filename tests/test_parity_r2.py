@@ -373,3 +373,47 @@ def test_zero_direction_reports_step_budget():
     ost, *_ = orc.render_into(t, 1.5, 1.5, 0.0, 0.0, np.zeros(0, np.uint8),
                               np.zeros(0, np.uint8), -1)
     assert st.value == ost == L.ST_STEP_BUDGET
+
+
+# ------------------------------------------------ chained multi-step launches
+@pytest.mark.parametrize("env,n,k,ring", [("my-way-home", 4096, 30, 3), ("key-door", 600, 25, 2),
+                                          ("health-gathering", 1000, 20, 4),
+                                          ("my-way-home", 20000, 6, 2)])
+def test_batch_steps_chained_equal_oracle(env, n, k, ring):
+    """tc.batch_steps: K step launches chained per CTA (no grid-wide wait
+    between them) == K reference steps: the final state, the last `ring`
+    steps' frames / rewards / dones from the output ring, bit-exact. The
+    20000-env case does not fit one wave (ordinary launches)."""
+    from paper_2605_19926_b200.engine import DeviceOut
+    spec = tc.make_env(env, max_steps=13)
+    seed = 21
+    bs = tc.batch_reset(spec, n, seed, device=DEV)
+    acts = tc.policy_actions(spec, n, 2 * k, seed)
+    outs = [DeviceOut.alloc(n, 64, 64, bs.device) for _ in range(ring)]
+    r = orc.Rollout(spec, n, seed)
+    # two calls back to back: epochs continue, the second call's first
+    # launch waits for the first call's last one
+    for part in range(2):
+        rows = torch.from_numpy(acts[part * k:(part + 1) * k]).to(DEV)
+        bs = tc.batch_steps(bs, rows, outs=outs)
+        snaps = {}
+        for s in range(k):
+            r.step(acts[part * k + s])
+            if s >= k - ring:
+                snaps[s] = (r.out["frames"].copy(), r.out["rewards"].copy(),
+                            r.out["dones"].copy())
+        torch.cuda.synchronize()
+        for s, (fr, rw, dn) in snaps.items():
+            o = outs[s % ring]
+            assert np.array_equal(o.frames.cpu().numpy(), fr), (part, s)
+            assert np.array_equal(o.rewards.cpu().numpy(), rw), (part, s)
+            assert np.array_equal(o.dones.cpu().numpy(), dn), (part, s)
+        host = bs.host_state()
+        for key, v in r.state.items():
+            assert np.array_equal(host[key], v), (part, key)
+        assert torch.equal(bs.frames, outs[(k - 1) % ring].frames)
+    bs.check()
+    # an ordinary step after a chain continues from the chained state
+    bs, rew, done = tc.batch_step(bs, acts[0], reuse=True)
+    r.step(acts[0])
+    assert np.array_equal(bs.frames.cpu().numpy(), r.out["frames"])
