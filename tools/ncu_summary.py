@@ -10,8 +10,10 @@ import sys
 
 rep, out = sys.argv[1], sys.argv[2]
 algo = float(sys.argv[3]) if len(sys.argv) > 3 else None
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
+# a report, or the `--page raw --csv` export of one (taken on the GPU box)
+raw = open(rep).read() if rep.endswith(".csv") else \
+    subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                   text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 d = dict(zip(hdr, vals))
