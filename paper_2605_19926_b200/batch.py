@@ -334,10 +334,13 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
         raise ContractError("action outside the spec's action set")
     rewards = stg.h_rew.copy()
     dones = stg.h_done.copy()
-    new = BatchState(spec=spec, n=bs.n, _ds=bs._ds, _sb=sb, _ob=ob, _counters=bs._counters,
-                     base=bs.base, n_total=bs.n_total,
-                     _retired=(bs._sb, bs._ob) if reuse else (), _stage=bs._stage,
-                     _chain=bs._chain)
+    # the successor: bs's fields with the new blocks (a __dict__ copy: this
+    # call is on the host's per-step critical path)
+    new = object.__new__(BatchState)
+    d = new.__dict__
+    d.update(bs.__dict__)
+    d["_sb"], d["_ob"] = sb, ob
+    d["_retired"] = (bs._sb, bs._ob) if reuse else ()
     if validate:
         new.check()
     return new, rewards, dones

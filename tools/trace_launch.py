@@ -38,11 +38,18 @@ torch.cuda.synchronize()
 graph = torch.cuda.CUDAGraph()
 cap = torch.cuda.Stream(dev)
 cap.wait_stream(torch.cuda.current_stream(dev))
+chained = len(sys.argv) > 3 and sys.argv[3] == "chained"
+if chained:
+    bsc = [tc.batch_steps(bs, torch.stack(acts[:3]), outs=outs[:3])]
+    torch.cuda.synchronize()
 with torch.cuda.stream(cap):
     with torch.cuda.graph(graph, stream=cap):
-        for s in range(K):
-            launch_batch(bs._ds, bs._sb, acts[3 + s], outs[3 + s], n, L.MODE_STEP, True, False,
-                         bs._counters)
+        if chained:
+            bsc[0] = tc.batch_steps(bsc[0], torch.stack(acts[3:3 + K]), outs=outs[3:3 + K])
+        else:
+            for s in range(K):
+                launch_batch(bs._ds, bs._sb, acts[3 + s], outs[3 + s], n, L.MODE_STEP, True,
+                             False, bs._counters)
 torch.cuda.synchronize()
 N.check(lib.tc_debug_trace_cta(buf.data_ptr()), "trace_cta")
 torch.cuda.synchronize()
