@@ -240,6 +240,26 @@ int tc_batch_step_mapped(const tc_spec *spec, const tc_state *state_in,
                          int32_t validate, tc_counters *counters_dev,
                          uint8_t *results_host, int32_t *flag_host, void *stream);
 
+/* tc_batch_step_mapped with its arguments in one struct, for bindings whose
+ * per-argument marshalling dominates a ~30 us step (Python ctypes: ~3 us for
+ * 12 arguments, ~0.5 us for one pointer). A step loop keeps one struct per
+ * (state_in, state_out) pair and passes it every step. */
+typedef struct tc_mapped_call {
+  const tc_spec *spec;
+  const tc_state *state_in;
+  const tc_state *state_out;
+  const int64_t *actions_host;
+  const tc_out *out;
+  int64_t n;
+  int32_t auto_reset;
+  int32_t validate;
+  tc_counters *counters_dev;
+  uint8_t *results_host;
+  int32_t *flag_host;
+  void *stream;
+} tc_mapped_call;
+int tc_batch_step_mapped_call(const tc_mapped_call *call);
+
 /* K fused steps in one launch with on-device uniform-random actions drawn
  * exactly as batch.policy_actions (batch.py:141-153) would draw them for
  * steps [step0, step0+K) of an (n_total)-env rollout whose env 0 is global

@@ -52,6 +52,14 @@ class TcCounters(C.Structure):
                 ("next_env", C.c_uint32), ("ctas_done", C.c_uint32), ("pad", C.c_uint32)]
 
 
+class TcMappedCall(C.Structure):
+    """tc_mapped_call: tc_batch_step_mapped's arguments in one struct."""
+    _fields_ = [("spec", _p), ("state_in", _p), ("state_out", _p), ("actions_host", _p),
+                ("out", _p), ("n", C.c_int64), ("auto_reset", C.c_int32),
+                ("validate", C.c_int32), ("counters_dev", _p), ("results_host", _p),
+                ("flag_host", _p), ("stream", _p)]
+
+
 class NativeError(RuntimeError):
     """A C-ABI call returned an error status."""
 
@@ -97,6 +105,7 @@ def _load() -> C.CDLL:
                                          C.c_int32, C.c_int32, _p, _p, _p, _p]),
         "tc_batch_step_mapped": (C.c_int, [_p, P(TcState), P(TcState), _p, P(TcOut), C.c_int64,
                                            C.c_int32, C.c_int32, _p, _p, _p, _p]),
+        "tc_batch_step_mapped_call": (C.c_int, [_p]),
         "tc_rollout": (C.c_int, [_p, P(TcState), P(TcOut), C.c_int64, C.c_int64, C.c_int64,
                                  C.c_uint64, C.c_int64, C.c_int32, C.c_int32, _p, _p]),
         "tc_seed_streams": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, _p, _p, _p]),

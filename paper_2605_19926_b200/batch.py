@@ -304,25 +304,27 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
         stg = bs._stage = _ActionStage(bs.n, bs.device)
     stg.h_act[:] = acts  # pinned, read by the kernel over the bus
     stg.h_flag[0] = 0
-    # the ctypes argument tuple of a (state in, state out) pair is built once
+    # the call struct of a (state in, state out) pair is built once; a step
+    # passes one pointer (tc_batch_step_mapped_call)
     key = (id(bs._sb), id(sb), id(ob), validate)
-    args = stg.calls.get(key)
-    if args is None:
-        args = (bs._ds.handle, N.C.byref(bs._sb.c_struct()), N.C.byref(sb.c_struct()),
-                stg.h_act_ptr, N.C.byref(ob.c_struct()), bs.n, 1, 1 if validate else 0,
-                N.ptr(bs._counters), stg.h_rew_ptr, stg.h_flag_ptr, stream_ptr(bs.device))
+    call = stg.calls.get(key)
+    if call is None:
+        si, so, oc = bs._sb.c_struct(), sb.c_struct(), ob.c_struct()
+        cs = N.TcMappedCall(bs._ds.handle.value, N.C.addressof(si), N.C.addressof(so),
+                            stg.h_act_ptr, N.C.addressof(oc), bs.n, 1, 1 if validate else 0,
+                            N.ptr(bs._counters), stg.h_rew_ptr, stg.h_flag_ptr,
+                            stream_ptr(bs.device))
         if len(stg.calls) > 8:
             stg.calls.clear()
-        stg.calls[key] = (args, bs._sb, sb, ob)  # keep the blocks alive with the key
-    else:
-        args = args[0]
+        # keep the structs and blocks alive with the key
+        stg.calls[key] = call = (N.C.addressof(cs), cs, si, so, oc, bs._sb, sb, ob)
     if stg.fn is None:
-        stg.fn = N.lib().tc_batch_step_mapped
+        stg.fn = N.lib().tc_batch_step_mapped_call
     if torch.cuda.current_device() == stg.dev_index:
-        rc = stg.fn(*args)
+        rc = stg.fn(call[0])
     else:
         with torch.cuda.device(bs.device):
-            rc = stg.fn(*args)
+            rc = stg.fn(call[0])
     if rc:
         N.check(rc, "tc_batch_step_mapped")
     if stg.h_flag[0]:

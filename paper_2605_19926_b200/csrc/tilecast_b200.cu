@@ -4071,6 +4071,13 @@ int tc_batch_step_mapped(const tc_spec* s, const tc_state* state_in, const tc_st
   return TC_OK;
 }
 
+int tc_batch_step_mapped_call(const tc_mapped_call* c) {
+  if (!c) return fail(TC_E_INVALID, "NULL call");
+  return tc_batch_step_mapped(c->spec, c->state_in, c->state_out, c->actions_host, c->out, c->n,
+                              c->auto_reset, c->validate, c->counters_dev, c->results_host,
+                              c->flag_host, c->stream);
+}
+
 // perf diagnostics of the mapped host step: mean host microseconds in the
 // launch call and in the wait for the completion word since the last reset
 int tc_debug_mapped_timing(double* out3, int32_t reset) {
