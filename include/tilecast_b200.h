@@ -178,16 +178,20 @@ int tc_batch_step_into(const tc_spec *spec, const tc_state *state_in,
                        int32_t validate, tc_counters *counters_dev, void *stream);
 
 /* K consecutive steps (K x batch_step, batch.py:109-138, auto-reset) as K
- * launches of the lean one-wave kernel with CTA-granular chaining instead of
- * a grid-wide wait between them: state ping-pongs a -> b -> a ..., step k
- * reads actions_dev[k * n .. k * n + n) and writes outs[k % ring]; the final
- * state is in b when k_steps is odd, else in a. flags_dev: device u32[2 * n]
+ * launches of the lean kernel chained per env instead of by a grid-wide
+ * wait between them: state ping-pongs a -> b -> a ..., step k reads
+ * actions_dev[k * n .. k * n + n) and writes outs[k % ring]; the final state
+ * is in b when k_steps is odd, else in a. flags_dev: device u32[2 * n]
  * zeroed once per batch; epoch0: a per-batch counter the caller advances by
- * k_steps per call (epochs are never reused). Env i of step k waits only for
- * its own state from step k - 1 (and for the step that last wrote
- * outs[k % ring]); the first step waits for all prior work on the stream, so
- * the action table may come from any earlier kernel. Batches that do not fit
- * one wave of the lean kernel get K ordinary launches. */
+ * k_steps per call (epochs are never reused). One-wave batches: env i of
+ * step k waits only for its own state from step k - 1 (and for the CTA of
+ * the step that last wrote outs[k % ring]). Multi-wave batches (env
+ * tickets): env i of step k waits for env i's whole step k - 1; each launch
+ * draws its tickets from its own slot of flags_dev[n ..), zeroed by a
+ * stream-ordered memset per run of n launches. The first step waits for all
+ * prior work on the stream, so the action table may come from any earlier
+ * kernel. Batches outside the lean kernels, and rings with debug taps, get
+ * K ordinary launches. */
 int tc_batch_steps(const tc_spec *spec, const tc_state *state_a,
                    const tc_state *state_b, const int64_t *actions_dev,
                    const tc_out *outs, int32_t ring, int64_t n, int32_t k_steps,

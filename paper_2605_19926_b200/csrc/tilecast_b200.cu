@@ -2803,7 +2803,13 @@ struct LeanSched {
   // done[] >= need_done (the output block it is about to overwrite was
   // finished), so a step's CTAs start as soon as the previous step's CTAs
   // free their slots instead of after its slowest CTA.
+  // Multi-wave (env tickets): ready[i] is published after env i's whole
+  // step (state and frames), so a later step's env i waits for nothing else
+  // (no per-CTA done epochs), and each launch draws its tickets from its own
+  // zeroed counter (`tickets`) instead of counters->next_env, which the
+  // previous launch's last CTA would otherwise still be re-zeroing.
   unsigned int* flags;
+  unsigned int* tickets;
   unsigned int epoch, need_ready, need_done;
 };
 
@@ -2858,7 +2864,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
 #if TC_TRACE
   if (g_trace_cta && threadIdx.x == 0) tcta[1] = gtime();
 #endif
-  const bool chained = ONE_WAVE && ls.flags != nullptr && ls.need_ready != 0;
+  const bool chained = ls.flags != nullptr && ls.need_ready != 0;
   if (!chained) asm volatile("griddepcontrol.wait;" ::: "memory");
 #if TC_TRACE
   if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
@@ -2873,7 +2879,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   constexpr size_t FB = (size_t)FW * FH * 3;
   const size_t frame_bytes = FB ? FB : (size_t)S.obs_h * S.obs_w * 3;
   bool first = true;
-  if (chained && i < n) {
+  if (ONE_WAVE && chained && i < n) {
     // this env's state from the previous step, and (need_done) the output
     // block this launch overwrites finished by the step that last wrote it
     if (lane == 0) {
@@ -2888,8 +2894,17 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   }
   while (i < n) {
     long long tnext = 0;
-    if (!ONE_WAVE && lane == 0 && counters)
-      tnext = ls.stride + (long long)atomicAdd(&counters->next_env, 1u);
+    if (!ONE_WAVE && lane == 0 && (counters || ls.flags))
+      tnext = ls.stride + (long long)atomicAdd(ls.flags ? ls.tickets : &counters->next_env, 1u);
+    if (!ONE_WAVE && chained) {
+      // multi-wave chained: env i's previous step (state and frames) is done
+      if (lane == 0) {
+        const volatile unsigned int* rd = ls.flags + i;
+        while ((int)(*rd - ls.need_ready) < 0) __nanosleep(64);
+      }
+      gr.sync();
+      __threadfence();
+    }
     if (!(ls.early && first)) act = actions[i];
     first = false;
     Env e;
@@ -2977,7 +2992,8 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     }
 #endif
     if (ONE_WAVE) break;
-    i = counters ? gr.shfl(tnext, 0) : i + ls.stride;
+    if (ls.flags) state_ready(gr, ls, i);  // multi-wave chained: the whole step
+    i = (counters || ls.flags) ? gr.shfl(tnext, 0) : i + ls.stride;
   }
 #if TC_TRACE
   if (g_trace_cta) {
@@ -2997,7 +3013,9 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   }
   // one wave: the mapped host step was released by ship_results as soon as
   // every env's reward / done had reached the host; nothing left to count
-  if (ONE_WAVE || !counters) return;
+  // (multi-wave chained launches draw tickets from their own counter: nothing
+  // to re-zero)
+  if (ONE_WAVE || !counters || ls.flags) return;
   {
     volatile int& s_last = *reinterpret_cast<int*>(smem);
     __syncthreads();
@@ -3668,6 +3686,7 @@ int tc_spec_destroy(tc_spec* s) {
 
 struct ChainArgs {
   unsigned int* flags;
+  unsigned int* tickets;  // multi-wave: this launch's zeroed ticket counter
   unsigned int epoch, need_ready, need_done;
 };
 
@@ -3719,13 +3738,14 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     ls.epc = one_wave ? (int)((n + grid - 1) / grid) : 0;
     ls.early = res_host != nullptr;
     ls.ctas = one_wave ? (int)((n + ls.epc - 1) / ls.epc) : 0;
-    ls.flags = nullptr;
+    ls.flags = ls.tickets = nullptr;
     ls.epoch = ls.need_ready = ls.need_done = 0;
-    if (chain && one_wave && !res_host) {
+    if (chain && !res_host) {
       ls.flags = chain->flags;
+      ls.tickets = chain->tickets;
       ls.epoch = chain->epoch;
       ls.need_ready = chain->need_ready;
-      ls.need_done = chain->need_done;
+      ls.need_done = one_wave ? chain->need_done : 0u;
     }
     const long long* acts = reinterpret_cast<const long long*>(actions_dev);
     int ar = auto_reset, va = validate;
@@ -3781,9 +3801,18 @@ int tc_batch_steps(const tc_spec* s, const tc_state* state_a, const tc_state* st
     return fail(TC_E_INVALID, "NULL state / actions / outs / flags");
   if (ring < 1 || k_steps < 0 || n < 0) return fail(TC_E_INVALID, "bad ring / k / n");
   if (k_steps == 0 || n == 0) return TC_OK;
-  // chaining needs the lean one-wave kernel (its fixed CTA -> env mapping);
-  // other batches get K ordinary launches
-  const bool chain_ok = s && s->dev.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA;
+  // chaining needs a lean kernel on every launch (one wave: its fixed CTA ->
+  // env mapping; multi-wave: env tickets with per-env epochs); other
+  // batches, and rings with debug taps (batch_kernel), get K ordinary launches
+  bool taps = false;
+  for (int r = 0; r < ring; r++)
+    taps = taps || outs[r].zbuf || outs[r].rayinfo || outs[r].spritevis;
+  const bool lean1 = s && s->dev.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA;
+  const bool lean2 = s && s->dev.lean && !lean1 && s->lean16_ctas > 0 && use_wide(s, n);
+  const bool chain_ok = !taps && (lean1 || lean2);
+  // multi-wave: launch k draws env tickets from flags[n + k % n], zeroed
+  // (stream-ordered after every earlier kernel) before each run of n launches
+  uint32_t* const tickets = flags_dev + n;
   for (int k = 0; k < k_steps; k++) {
     const tc_state* in = (k & 1) ? state_b : state_a;
     const tc_state* outst = (k & 1) ? state_a : state_b;
@@ -3795,6 +3824,12 @@ int tc_batch_steps(const tc_spec* s, const tc_state* state_a, const tc_state* st
     // wraps, for the step that last wrote the output block it overwrites
     ca.need_ready = k == 0 ? 0u : ca.epoch - 1u;
     ca.need_done = (k >= ring) ? ca.epoch - (uint32_t)ring : 0u;
+    ca.tickets = tickets + (k % n);
+    if (chain_ok && lean2 && k % n == 0) {
+      const int64_t run = std::min<int64_t>(n, (int64_t)k_steps - k);
+      TC_CUDA(cudaMemsetAsync(tickets, 0, (size_t)run * 4, (cudaStream_t)stream));
+      ca.need_ready = 0u;  // the memset already ordered this launch after the last
+    }
     const int rc = launch_batch_kernel(s, in, outst, actions_dev + (size_t)k * (size_t)n,
                                        &outs[k % ring], n, TC_MODE_STEP, auto_reset, validate,
                                        counters_dev, stream, nullptr, nullptr,

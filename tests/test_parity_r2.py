@@ -376,20 +376,28 @@ def test_zero_direction_reports_step_budget():
 
 
 # ------------------------------------------------ chained multi-step launches
-@pytest.mark.parametrize("env,n,k,ring", [("my-way-home", 4096, 30, 3), ("key-door", 600, 25, 2),
-                                          ("health-gathering", 1000, 20, 4),
-                                          ("my-way-home", 20000, 6, 2)])
-def test_batch_steps_chained_equal_oracle(env, n, k, ring):
-    """tc.batch_steps: K step launches chained per CTA (no grid-wide wait
-    between them) == K reference steps: the final state, the last `ring`
-    steps' frames / rewards / dones from the output ring, bit-exact. The
-    20000-env case does not fit one wave (ordinary launches)."""
+@pytest.mark.parametrize("env,n,k,ring,taps", [
+    ("my-way-home", 4096, 30, 3, False), ("key-door", 600, 25, 2, False),
+    ("health-gathering", 1000, 20, 4, False), ("my-way-home", 20000, 6, 2, False),
+    ("key-door", 16384, 12, 2, False), ("key-door", 9000, 10, 1, False),
+    ("dmlab-static-03@128", 8192, 6, 2, False), ("my-way-home", 4096, 6, 2, True)])
+def test_batch_steps_chained_equal_oracle(env, n, k, ring, taps):
+    """tc.batch_steps: K step launches chained per env / CTA (no grid-wide
+    wait between them) == K reference steps: the final state, the last
+    `ring` steps' frames / rewards / dones from the output ring, bit-exact.
+    One-wave batches chain per CTA; multi-wave ones (20000, 16384, 9000 envs
+    at 64x64, 8192 at 128x128) per env with per-launch ticket counters, ring
+    1 included (every step rewrites the same block); a ring with a debug-tap
+    block runs K ordinary launches (the tapped kernel does not chain)."""
     from paper_2605_19926_b200.engine import DeviceOut
-    spec = tc.make_env(env, max_steps=13)
+    env, _, obs = env.partition("@")
+    size = {"obs_width": int(obs), "obs_height": int(obs)} if obs else {}
+    spec = tc.make_env(env, max_steps=13, **size)
     seed = 21
     bs = tc.batch_reset(spec, n, seed, device=DEV)
     acts = tc.policy_actions(spec, n, 2 * k, seed)
-    outs = [DeviceOut.alloc(n, 64, 64, bs.device) for _ in range(ring)]
+    oh, ow = spec.tables.obs_height, spec.tables.obs_width
+    outs = [DeviceOut.alloc(n, oh, ow, bs.device, debug=taps and r == 0) for r in range(ring)]
     r = orc.Rollout(spec, n, seed)
     # two calls back to back: epochs continue, the second call's first
     # launch waits for the first call's last one
