@@ -3509,6 +3509,22 @@ bool use_wide(const tc_spec* s, int64_t n) {
   return n > (int64_t)s->max_ctas * per_cta;
 }
 
+// which kernel steps n envs: 1 = lean, one env per warp, one wave; 2 = lean
+// multi-wave (env tickets); 0 = batch_kernel. (A batch past one wave of the
+// lean kernel that still fits one wave of the 128-register batch_kernel runs
+// there: measured +7 % on the 160x128-tile map; TILECAST_LEAN2_ANY=1 sends it
+// to the multi-wave lean kernel instead, for experiments.)
+int lean_kind(const tc_spec* s, int64_t n) {
+  const SpecDev& d = s->dev;
+  if (!d.lean) return 0;
+  if (n <= (int64_t)s->lean_ctas * WARPS_PER_CTA) return 1;
+  static const bool any_n = [] {
+    const char* e = getenv("TILECAST_LEAN2_ANY");
+    return e && atoi(e) != 0;
+  }();
+  return (s->lean16_ctas > 0 && (use_wide(s, n) || any_n)) ? 2 : 0;
+}
+
 int grid_for(const tc_spec* s, int64_t n, bool wide = false) {
   const int per_cta = WARPS_PER_CTA * (32 / s->dev.group);  // envs per CTA pass
   const int64_t want = (n + per_cta - 1) / per_cta;
@@ -3559,9 +3575,9 @@ const char* tc_build_info(void) {
 const char* tc_step_kernel(const tc_spec* s, int64_t n) {
   if (!s) return "none";
   const SpecDev& d = s->dev;
-  if (d.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA)
-    return "lean_kernel (one env per warp, one wave, 72 registers)";
-  if (d.lean && s->lean16_ctas > 0 && use_wide(s, n))
+  const int lk = lean_kind(s, n);
+  if (lk == 1) return "lean_kernel (one env per warp, one wave, 72 registers)";
+  if (lk == 2)
     return d.obs_w <= 64 ? "lean_kernel (two envs per warp, multi-wave env tickets, 96 registers)"
                          : "lean_kernel (one env per warp, multi-wave env tickets, 72 registers)";
   if (use_wide(s, n))
@@ -3717,11 +3733,8 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
   // the lean kernels: one env per warp for batches that fit one wave of it
   // (latency-bound), two envs per warp over a full wave with env tickets for
   // larger batches (issue-bound: the pair shares its convergent code)
-  const int64_t lean_cap = (int64_t)s->lean_ctas * WARPS_PER_CTA;
-  const bool lean1 = d.lean && n <= lean_cap;
-  // (a batch that still fits one wave of the two-envs-per-warp batch_kernel
-  // at 128 registers runs there: measured +7 % on the 160x128-tile map)
-  const bool lean2 = d.lean && !lean1 && s->lean16_ctas > 0 && use_wide(s, n);
+  const int lk = lean_kind(s, n);
+  const bool lean1 = lk == 1, lean2 = lk == 2;
   if (mode == TC_MODE_STEP && !taps && (lean1 || lean2)) {
     const int per_cta = lean_per_cta(d.obs_w, lean1);
     const int64_t want = (n + per_cta - 1) / per_cta;
@@ -3807,8 +3820,8 @@ int tc_batch_steps(const tc_spec* s, const tc_state* state_a, const tc_state* st
   bool taps = false;
   for (int r = 0; r < ring; r++)
     taps = taps || outs[r].zbuf || outs[r].rayinfo || outs[r].spritevis;
-  const bool lean1 = s && s->dev.lean && n <= (int64_t)s->lean_ctas * WARPS_PER_CTA;
-  const bool lean2 = s && s->dev.lean && !lean1 && s->lean16_ctas > 0 && use_wide(s, n);
+  const int lk = s ? lean_kind(s, n) : 0;
+  const bool lean1 = lk == 1, lean2 = lk == 2;
   const bool chain_ok = !taps && (lean1 || lean2);
   // multi-wave: launch k draws env tickets from flags[n + k % n], zeroed
   // (stream-ordered after every earlier kernel) before each run of n launches
