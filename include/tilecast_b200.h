@@ -191,7 +191,8 @@ int tc_batch_step_into(const tc_spec *spec, const tc_state *state_in,
  * stream-ordered memset per run of n launches. The first step waits for all
  * prior work on the stream, so the action table may come from any earlier
  * kernel. Batches outside the lean kernels, and rings with debug taps, get
- * K ordinary launches. */
+ * K ordinary launches, and so do multi-wave batches more than 4 waves deep
+ * (their launch tails are negligible; the per-env epochs are not). */
 int tc_batch_steps(const tc_spec *spec, const tc_state *state_a,
                    const tc_state *state_b, const int64_t *actions_dev,
                    const tc_out *outs, int32_t ring, int64_t n, int32_t k_steps,

@@ -88,6 +88,7 @@ constexpr int WARPS_PER_CTA = 4;
 constexpr int BAND_BYTES_TARGET = 3072;       // per staging buffer
 constexpr int CTA_SCRATCH = 160;               // step kernel per-CTA scratch bytes
 constexpr int SMEM_MAP_MAX_CELLS = 4096;      // stage map in smem up to this
+constexpr int CHAIN_MAX_WAVES = 4;            // tc_batch_steps chains multi-wave batches up to this
 constexpr int SMEM_U8_MAX_BYTES = 48 * 1024;  // u8 stop codes (+ tables) staged up to this
 
 // packed cell word: bits 0-7 = wall colour or door index, 8-9 = cell tag,
@@ -3517,6 +3518,11 @@ bool use_wide(const tc_spec* s, int64_t n) {
 int lean_kind(const tc_spec* s, int64_t n) {
   const SpecDev& d = s->dev;
   if (!d.lean) return 0;
+  static const int force = [] {
+    const char* e = getenv("TILECAST_LEAN_KIND");
+    return e ? atoi(e) : -1;
+  }();
+  if (force == 2 && s->lean16_ctas > 0) return 2;
   if (n <= (int64_t)s->lean_ctas * WARPS_PER_CTA) return 1;
   static const bool any_n = [] {
     const char* e = getenv("TILECAST_LEAN2_ANY");
@@ -3822,7 +3828,12 @@ int tc_batch_steps(const tc_spec* s, const tc_state* state_a, const tc_state* st
     taps = taps || outs[r].zbuf || outs[r].rayinfo || outs[r].spritevis;
   const int lk = s ? lean_kind(s, n) : 0;
   const bool lean1 = lk == 1, lean2 = lk == 2;
-  const bool chain_ok = !taps && (lean1 || lean2);
+  // (multi-wave: only while the batch is a few waves deep -- chaining hides
+  // the tail of each launch, but costs every env a device-scope fence after
+  // its frame; at 2^20 envs, ~180 waves, the tail is < 1 % and the fences
+  // cost ~20 %)
+  const int64_t slots = lean2 ? (int64_t)s->lean16_ctas * lean_per_cta(s->dev.obs_w, false) : 0;
+  const bool chain_ok = !taps && (lean1 || (lean2 && n <= CHAIN_MAX_WAVES * slots));
   // multi-wave: launch k draws env tickets from flags[n + k % n], zeroed
   // (stream-ordered after every earlier kernel) before each run of n launches
   uint32_t* const tickets = flags_dev + n;
