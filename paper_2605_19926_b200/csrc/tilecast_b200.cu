@@ -2370,7 +2370,23 @@ __device__ __forceinline__ void stage_map(const SpecDev& S, uint32_t* smap, cons
 }
 
 
-// MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387
+// multi-wave mapped step, last CTA: the [rewards | dones] block to pinned host
+// memory, 8 independent 16-byte loads in flight per thread (the copy is
+// bound by the loads' round trip, not by the bus)
+__device__ __forceinline__ void copy_results_host(const uint4* src, uint4* dst, size_t nv) {
+  constexpr int U = 8;
+  const size_t step = (size_t)blockDim.x * U;
+  size_t k = threadIdx.x;
+  for (; k + (U - 1) * blockDim.x < nv; k += step) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = __ldcg(src + k + (size_t)u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < U; u++) dst[k + (size_t)u * blockDim.x] = v[u];
+  }
+  for (; k < nv; k += blockDim.x) dst[k] = __ldcg(src + k);
+}
+
 // MODE_RESET / MODE_STEP / MODE_RENDER over envs [0, n), _pycore.py:346-387.
 // A group of G lanes owns one env at a time (G = 32: a warp; G = 16: each
 // half of a warp runs its own env).
@@ -2585,9 +2601,8 @@ __device__ __forceinline__ void batch_body(const SpecDev& S, const StateDev& st,
       // ship them to pinned host memory with 16-byte coalesced stores
       __threadfence();
       const size_t bytes = (size_t)n * 9, nv = bytes >> 4;
-      const uint4* src = reinterpret_cast<const uint4*>(out.rewards);
-      uint4* dst = reinterpret_cast<uint4*>(out.res_host);
-      for (size_t k = threadIdx.x; k < nv; k += blockDim.x) dst[k] = __ldcg(src + k);
+      copy_results_host(reinterpret_cast<const uint4*>(out.rewards),
+                        reinterpret_cast<uint4*>(out.res_host), nv);
       const uint8_t* sb = reinterpret_cast<const uint8_t*>(out.rewards);
       for (size_t k = nv * 16 + threadIdx.x; k < bytes; k += blockDim.x)
         out.res_host[k] = __ldcg(sb + k);
@@ -2858,8 +2873,14 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   const int map_bytes = map_smem_bytes(S);
   // mapped host path: the host wrote the actions before the launch (see
   // batch_kernel); device actions are read after griddepcontrol.wait
-  long long act = 0;
+  long long act = 0, act_next = 0;
   if (ls.early && i < n) act = actions[i];
+  // multi-wave mapped: the next ticket's action is read from host memory one
+  // env ahead (after this env's dynamics), so its bus round trip overlaps
+  // the render instead of stalling the warp at the top of every env
+  const auto prefetch = [&](long long tn) {
+    if (!ONE_WAVE && ls.early && lane == 0 && tn < n) act_next = actions[tn];
+  };
   stage_map_issue(S, smap, cell, solid);
   stage_map_wait();
 #if TC_TRACE
@@ -2906,7 +2927,11 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
       gr.sync();
       __threadfence();
     }
-    if (!(ls.early && first)) act = actions[i];
+    if (!ls.early) {
+      act = actions[i];
+    } else if (!first) {
+      act = gr.shfl(act_next, 0);
+    }
     first = false;
     Env e;
     TRACE(i, 0);
@@ -2930,9 +2955,11 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
       }
       if (ONE_WAVE && out.res_host)
         ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
+      prefetch(tnext);
     } else {
       TRACE(i, 1);
       const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
+      prefetch(tnext);
       if (lane == 0) {
         out.rewards[i] = o.reward;
         out.dones[i] = (uint8_t)o.done;
@@ -3038,9 +3065,8 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     } else if (s_last && out.res_host) {
       __threadfence();
       const size_t bytes = (size_t)n * 9, nv = bytes >> 4;
-      const uint4* src = reinterpret_cast<const uint4*>(out.rewards);
-      uint4* dst = reinterpret_cast<uint4*>(out.res_host);
-      for (size_t k = threadIdx.x; k < nv; k += blockDim.x) dst[k] = __ldcg(src + k);
+      copy_results_host(reinterpret_cast<const uint4*>(out.rewards),
+                        reinterpret_cast<uint4*>(out.res_host), nv);
       const uint8_t* sb = reinterpret_cast<const uint8_t*>(out.rewards);
       for (size_t k = nv * 16 + threadIdx.x; k < bytes; k += blockDim.x)
         out.res_host[k] = __ldcg(sb + k);
