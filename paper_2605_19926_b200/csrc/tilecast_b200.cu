@@ -2894,6 +2894,10 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   const WarpSmem sm = carve(smem + map_bytes + grp * S.warp_smem);
   double* rew_s = reinterpret_cast<double*>(smem + map_bytes + PER_CTA * S.warp_smem);
   uint8_t* done_s = reinterpret_cast<uint8_t*>(rew_s + PER_CTA);
+  // the env's goal entity parks here across the wall pass (only the sprite
+  // cull reads it after the dynamics): a register there would be spilled
+  int* agoal_s = reinterpret_cast<int*>(rew_s + 2 * PER_CTA);
+  static_assert(20 * PER_CTA <= CTA_SCRATCH, "CTA scratch: rewards, dones, goals");
   // one wave, mapped: warps without an env still take part in the CTA's
   // result hand-off barrier
   if (ONE_WAVE && out.res_host && i >= n)
@@ -2980,6 +2984,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
       if (o.done && auto_reset) reset_draws(S, e);
       store_env<G>(S, so, i, e);
       if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
+      if (lane == 0) agoal_s[grp] = e.agoal;
       TRACE(i, 2);
       uint8_t* frame = out.frames + (size_t)i * frame_bytes;
       const double planex = -e.dy * PLANE_HALF_WIDTH;
@@ -2998,6 +3003,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
       gr.sync();
       TRACE(i, 3);
       if (status == TC_ST_OK) {
+        e.agoal = agoal_s[grp];  // (the wall pass synced the group)
         const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
         TRACE(i, 4);
 #if TC_TRACE
