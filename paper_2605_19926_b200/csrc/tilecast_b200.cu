@@ -3293,6 +3293,10 @@ const void* select_rollout(int nc, int group) {
   }
 }
 
+#ifndef TC_MIN_CTAS_LEAN128W
+#define TC_MIN_CTAS_LEAN128W 5  // lean kernel, 128x128 frames, multi-wave: 96 registers
+                                // (7 spill slots instead of 43; +3 % over 7 CTAs at 72)
+#endif
 #ifndef TC_MIN_CTAS_LEAN16
 #define TC_MIN_CTAS_LEAN16 5  // lean kernel, two envs per warp (multi-wave): 96 registers
 #endif
@@ -3308,7 +3312,8 @@ const void* select_lean_t(int w, int h) {
   }
   if (w == 64 && h == 64) return (const void*)lean_kernel<2, ONE_WAVE, 64, 64, 32, TC_MIN_CTAS_LEAN>;
   if (w == 128 && h == 128)
-    return (const void*)lean_kernel<4, ONE_WAVE, 128, 128, 32, TC_MIN_CTAS_LEAN>;
+    return ONE_WAVE ? (const void*)lean_kernel<4, ONE_WAVE, 128, 128, 32, TC_MIN_CTAS_LEAN>
+                    : (const void*)lean_kernel<4, ONE_WAVE, 128, 128, 32, TC_MIN_CTAS_LEAN128W>;
   switch (w / 32) {
     case 1: return (const void*)lean_kernel<1, ONE_WAVE, 0, 0, 32, TC_MIN_CTAS_LEAN>;
     case 2: return (const void*)lean_kernel<2, ONE_WAVE, 0, 0, 32, TC_MIN_CTAS_LEAN>;
