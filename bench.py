@@ -485,6 +485,7 @@ def main():
     eb = tc.batch_reset(spec, n, seed + 1, device=dev, base=base, n_total=n_total)
     for s in range(3):
         eb, rh, dh = tc.batch_step_host(eb, host_acts[s], reuse=True)
+    tc.pipeline_drain()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -495,6 +496,9 @@ def main():
     for s in range(args.e2e_steps):
         eb, rh, dh = tc.batch_step_host(eb, host_acts[3 + s], reuse=True)
         np.add(racc, rh, out=racc)
+    # the loop is over: cancel the step launched ahead of actions that will
+    # not come (pipelined host step), then wait for the device
+    tc.pipeline_drain()
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
     rsum = float(racc.sum())

@@ -265,6 +265,42 @@ typedef struct tc_mapped_call {
 } tc_mapped_call;
 int tc_batch_step_mapped_call(const tc_mapped_call *call);
 
+/* Pipelined host step loop: batch_step(bs, actions, reuse=True)
+ * (batch.py:109-138) over host buffers, one step per call, like
+ * tc_batch_step_mapped_call -- plus, before waiting for this step's results,
+ * it launches the NEXT step of the reuse=True ping-pong (input = this step's
+ * state_out, output = this step's state_in, output block = next_out) behind
+ * a gate: that launch stages its tables, waits for this step's grid, then
+ * waits for the host. The next call whose arguments match releases it with
+ * one store to host memory instead of launching (the caller has already
+ * written that step's actions), so the launch call, the launch latency and
+ * this step's frame rendering leave the host's per-step critical path.
+ * flag_host is int32[8] (16-byte aligned): [0] bad action, [1] results
+ * ready (as tc_batch_step_mapped), [4] / [5] the gate's go / cancel words,
+ * [6] expired mark -- all managed by the call except [0]. gate_dev is one
+ * zeroed device uint32 per action stage. A call that does not match the
+ * pending launch (other buffers, another batch) cancels it first, as does
+ * every other library launch; a watchdog thread cancels a launch nobody
+ * released within TILECAST_PIPE_TIMEOUT_US (default 1000 us), so work queued
+ * behind it waits at most that long. A cancelled launch exits without any
+ * effect. speculate = 0 makes this exactly tc_batch_step_mapped_call.
+ * (No reference counterpart: the reference's batch_step is synchronous CPU
+ * code; this is the same step sequence with the launch moved earlier.) */
+typedef struct tc_pipe_call {
+  tc_mapped_call step;
+  const tc_out *next_out;
+  uint32_t *gate_dev;
+  int32_t speculate;
+  int32_t pad;
+} tc_pipe_call;
+int tc_batch_step_pipelined(const tc_pipe_call *call);
+/* Cancel a pending pipelined launch (no-op if none). */
+int tc_pipe_cancel(void);
+/* Cancel a pending launch and clear the timeout back-off. */
+int tc_pipe_reset(void);
+/* Pipeline counters: [released, cancelled, of which timeouts, pending]. */
+int tc_pipe_stats(uint64_t *out4);
+
 /* K fused steps in one launch with on-device uniform-random actions drawn
  * exactly as batch.policy_actions (batch.py:141-153) would draw them for
  * steps [step0, step0+K) of an (n_total)-env rollout whose env 0 is global

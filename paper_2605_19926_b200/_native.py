@@ -60,6 +60,12 @@ class TcMappedCall(C.Structure):
                 ("flag_host", _p), ("stream", _p)]
 
 
+class TcPipeCall(C.Structure):
+    """tc_pipe_call: a mapped step plus the successor's output block and gate."""
+    _fields_ = [("step", TcMappedCall), ("next_out", _p), ("gate_dev", _p),
+                ("speculate", C.c_int32), ("pad", C.c_int32)]
+
+
 class NativeError(RuntimeError):
     """A C-ABI call returned an error status."""
 
@@ -106,6 +112,10 @@ def _load() -> C.CDLL:
         "tc_batch_step_mapped": (C.c_int, [_p, P(TcState), P(TcState), _p, P(TcOut), C.c_int64,
                                            C.c_int32, C.c_int32, _p, _p, _p, _p]),
         "tc_batch_step_mapped_call": (C.c_int, [_p]),
+        "tc_batch_step_pipelined": (C.c_int, [_p]),
+        "tc_pipe_cancel": (C.c_int, []),
+        "tc_pipe_reset": (C.c_int, []),
+        "tc_pipe_stats": (C.c_int, [_p]),
         "tc_rollout": (C.c_int, [_p, P(TcState), P(TcOut), C.c_int64, C.c_int64, C.c_int64,
                                  C.c_uint64, C.c_int64, C.c_int32, C.c_int32, _p, _p]),
         "tc_seed_streams": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, _p, _p, _p]),
@@ -137,7 +147,31 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is None:
         _lib = _load()
+        # a pipelined step still waiting for its actions would hold the GPU
+        # until the watchdog's timeout at interpreter exit
+        import atexit
+        atexit.register(pipe_cancel)
     return _lib
+
+
+def pipe_cancel() -> None:
+    """Cancel a pending pipelined step launch (batch_step_host with
+    ``reuse=True``), if any: its kernel exits without effect. Cheap when
+    nothing is pending."""
+    if _lib is not None:
+        _lib.tc_pipe_cancel()
+
+
+def pipe_reset() -> None:
+    """Cancel a pending pipelined launch and clear the watchdog back-off."""
+    lib().tc_pipe_reset()
+
+
+def pipe_stats() -> dict:
+    """Pipelined-step counters of this process."""
+    out = (C.c_uint64 * 4)()
+    lib().tc_pipe_stats(out)
+    return {"released": out[0], "cancelled": out[1], "timeouts": out[2], "pending": out[3]}
 
 
 def check(rc: int, what: str) -> None:

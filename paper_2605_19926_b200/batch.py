@@ -71,10 +71,12 @@ class BatchState:
     @property
     def frames(self) -> torch.Tensor:
         """(n, obs_height, obs_width, 3) uint8 observations in HBM."""
+        N.pipe_cancel()  # work on these tensors must not queue behind a gated launch
         return self._ob.frames
 
     def check(self) -> None:
         """Raise for faults accumulated on the device since the batch began."""
+        N.pipe_cancel()
         viol, bad = read_counters(self._counters)
         if bad & (1 << L.ST_BAD_ACTION):
             raise ContractError(
@@ -87,6 +89,7 @@ class BatchState:
             raise RuntimeError(f"collision invariant violated in {viol} environment step(s)")
 
     def host_state(self) -> dict:
+        N.pipe_cancel()
         return self._sb.to_host()
 
     def state(self, i: int) -> EnvState:
@@ -111,6 +114,7 @@ class BatchState:
 
     @property
     def last_events(self) -> np.ndarray:
+        N.pipe_cancel()
         return self._ob.events.cpu().numpy().view(np.uint32)
 
 
@@ -134,7 +138,10 @@ class _ActionStage:
         res = self._h_res.numpy()
         self.h_rew = res[:8 * n].view(np.float64)
         self.h_done = res[8 * n:].view(np.bool_)
-        self._h_flag = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        # [0] bad action, [1] results ready, [4] / [5] pipelined gate go /
+        # cancel, [6] expired (tc_batch_step_pipelined)
+        self._h_flag = torch.zeros(8, dtype=torch.int32, pin_memory=True)
+        self.gate_dev = torch.zeros(1, dtype=torch.int32, device=device)
         self.h_flag = self._h_flag.numpy()
         self.h_flag_ptr = self._h_flag.data_ptr()
         self.h_act_ptr = self._h_act.data_ptr()
@@ -278,7 +285,8 @@ def _check_host_actions(bs: BatchState, actions) -> np.ndarray:
 
 
 def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
-                    reuse: bool = False) -> tuple[BatchState, np.ndarray, np.ndarray]:
+                    reuse: bool = False, pipeline: bool = True
+                    ) -> tuple[BatchState, np.ndarray, np.ndarray]:
     """batch_step with the reference's return types: host actions in, numpy
     ``(rewards f64[N], dones bool[N])`` out (batch.py:136-138), the state and
     frames staying on the GPU. One native call (tc_batch_step_mapped): the
@@ -286,7 +294,14 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
     last CTA writes rewards / dones back to pinned host memory; no copy-engine
     transfers, one launch, one synchronisation. The reference's action
     contract (batch.py:92-106) is checked by the kernel: a violation leaves
-    ``bs`` untouched and raises the reference's ContractError."""
+    ``bs`` untouched and raises the reference's ContractError.
+
+    With ``reuse=True`` (and ``pipeline``) the call also launches the next
+    step of the ping-pong before waiting for this one's results
+    (tc_batch_step_pipelined): the next ``batch_step_host(new, ...,
+    reuse=True)`` only writes its actions and opens that launch's gate. Any
+    other use of the batch or the library cancels the waiting launch (see
+    ``pipeline_drain``); it never changes results."""
     spec, t = bs.spec, bs.spec.tables
     acts = actions if (type(actions) is np.ndarray and actions.dtype == np.int64
                        and actions.flags.c_contiguous) else \
@@ -306,20 +321,24 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
     stg.h_flag[0] = 0
     # the call struct of a (state in, state out) pair is built once; a step
     # passes one pointer (tc_batch_step_mapped_call)
-    key = (id(bs._sb), id(sb), id(ob), validate)
+    # the successor of a reuse=True step writes this step's input state and
+    # bs's output block: the pipelined call launches it ahead of its actions
+    spec_next = bool(reuse and pipeline)
+    key = (id(bs._sb), id(sb), id(ob), validate, id(bs._ob), spec_next)
     call = stg.calls.get(key)
     if call is None:
-        si, so, oc = bs._sb.c_struct(), sb.c_struct(), ob.c_struct()
-        cs = N.TcMappedCall(bs._ds.handle.value, N.C.addressof(si), N.C.addressof(so),
-                            stg.h_act_ptr, N.C.addressof(oc), bs.n, 1, 1 if validate else 0,
-                            N.ptr(bs._counters), stg.h_rew_ptr, stg.h_flag_ptr,
-                            stream_ptr(bs.device))
+        si, so, oc, nc = bs._sb.c_struct(), sb.c_struct(), ob.c_struct(), bs._ob.c_struct()
+        cs = N.TcPipeCall(N.TcMappedCall(bs._ds.handle.value, N.C.addressof(si),
+                                         N.C.addressof(so), stg.h_act_ptr, N.C.addressof(oc),
+                                         bs.n, 1, 1 if validate else 0, N.ptr(bs._counters),
+                                         stg.h_rew_ptr, stg.h_flag_ptr, stream_ptr(bs.device)),
+                          N.C.addressof(nc), stg.gate_dev.data_ptr(), 1 if spec_next else 0, 0)
         if len(stg.calls) > 8:
             stg.calls.clear()
         # keep the structs and blocks alive with the key
-        stg.calls[key] = call = (N.C.addressof(cs), cs, si, so, oc, bs._sb, sb, ob)
+        stg.calls[key] = call = (N.C.addressof(cs), cs, si, so, oc, nc, bs._sb, sb, ob, bs._ob)
     if stg.fn is None:
-        stg.fn = N.lib().tc_batch_step_mapped_call
+        stg.fn = N.lib().tc_batch_step_pipelined
     if torch.cuda.current_device() == stg.dev_index:
         rc = stg.fn(call[0])
     else:
@@ -346,6 +365,14 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
     if validate:
         new.check()
     return new, rewards, dones
+
+
+def pipeline_drain() -> None:
+    """End a ``batch_step_host(..., reuse=True)`` loop: cancel the step
+    launched ahead of its actions (it exits without effect), so work queued
+    on the stream after it runs at once instead of after the watchdog's
+    timeout. Accessing a batch's frames / state does this implicitly."""
+    N.pipe_cancel()
 
 
 def batch_step(bs: BatchState, actions: Sequence[Action | int] | np.ndarray | torch.Tensor, *,

@@ -29,7 +29,7 @@ def _host_fingerprint() -> dict:
 
 def bench(env_id: str, n: int, steps: int, seed: int, width: int, height: int) -> dict:
     from . import batch_reset, make_env, policy_actions, registered_ids, rollout
-    from .batch import batch_step_host
+    from .batch import batch_step_host, pipeline_drain
     if env_id not in registered_ids():
         raise SystemExit(f"error: unknown environment {env_id!r}; valid ids: "
                          f"{', '.join(registered_ids())}")
@@ -40,10 +40,12 @@ def bench(env_id: str, n: int, steps: int, seed: int, width: int, height: int) -
     bs = batch_reset(spec, n, seed)
     for s in range(3):
         bs, _, _ = batch_step_host(bs, acts[s], reuse=True)
+    pipeline_drain()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for s in range(steps):
         bs, _, _ = batch_step_host(bs, acts[3 + s], reuse=True)
+    pipeline_drain()
     torch.cuda.synchronize()
     rate = n * steps / (time.perf_counter() - t0)
     # untimed rollout for the reward accounting (cli.py:76-81)

@@ -34,6 +34,9 @@
 #include <mutex>
 #include <string>
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -2827,7 +2830,79 @@ struct LeanSched {
   unsigned int* flags;
   unsigned int* tickets;
   unsigned int epoch, need_ready, need_done;
+  // Pipelined host step (tc_batch_step_pipelined): a launch made one step
+  // ahead of its actions. After the previous grid (griddepcontrol.wait) and
+  // the spec staging, CTA 0 polls the host gate words [go | cancel] (pinned,
+  // written by the host) for gate_q and publishes the outcome to gate_dev
+  // (2q = go, 2q + 1 = cancel); the other CTAs poll gate_dev in L2. A
+  // cancelled launch exits before touching any state or output.
+  unsigned int* gate_dev;
+  const unsigned long long* gate_host;
+  unsigned int gate_q;
+  // resident host-step loop (lean_kernel RES = true): after step k the
+  // kernel waits at gate gate_q + k + 1 for step k + 1 of the reuse=True
+  // ping-pong (state blocks swap, output blocks alternate out / out2)
+  // instead of exiting; a cancel ends it with every state block as an
+  // ordinary launch sequence would have left it
+  OutDev out2;
 };
+
+// the pipelined step's gate (see LeanSched): true = released (the host's
+// actions for this step are in pinned memory), false = cancelled. A launch
+// nobody releases or cancels within ~1 s cancels itself and leaves an
+// "expired" mark in the host word after the gate pair (a host that released
+// it then sees the kernel finish without results and reports the error).
+__device__ __forceinline__ unsigned long long gate_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// host-written data read after the gate (the actions): ordinary loads. The
+// gate is a causality chain -- host stores actions, then go (x86 TSO); CTA 0
+// observes go with an acquire.sys load and publishes it with a release.gpu
+// store; every other CTA acquires that store -- so the loads after it see
+// the host's actions. (A relaxed.sys load per warp instead costs ~140 us per
+// step at 4096 envs, measured: sys-scope loads of pinned memory serialise.)
+__device__ __forceinline__ long long ld_sys(const long long* p) { return *p; }
+__device__ __noinline__ bool gate_pass(const LeanSched& ls, unsigned int q) {
+  bool go = false;
+  if (threadIdx.x == 0) {
+    const unsigned int q2 = 2u * q;
+    unsigned int w;
+    if (blockIdx.x == 0) {
+      const unsigned long long t0 = gate_clock();
+      for (unsigned int spin = 0;; spin++) {
+        unsigned long long hw;
+#if TC_GATE_POLL == 1
+        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(hw) : "l"(ls.gate_host) : "memory");
+#else
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(hw) : "l"(ls.gate_host) : "memory");
+#endif
+        if ((unsigned int)hw == q) { w = q2; break; }
+        if ((unsigned int)(hw >> 32) == q) { w = q2 + 1u; break; }
+        if ((spin & 255u) == 255u && gate_clock() - t0 > 1000000000ull) {
+          w = q2 + 1u;
+          *(volatile unsigned int*)(ls.gate_host + 1) = q;
+          __threadfence_system();
+          break;
+        }
+        __nanosleep(64);
+      }
+#if TC_GATE_POLL == 1
+      __threadfence_system();  // fence-based acquire of the host's stores
+#endif
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ls.gate_dev), "r"(w) : "memory");
+    } else {
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(w) : "l"(ls.gate_dev) : "memory");
+        if ((int)(w - q2) >= 0) break;
+        __nanosleep(100);
+      }
+    }
+    go = w == q2;
+  }
+  return __syncthreads_or(go) != 0;
+}
 
 // chained steps: env i's state is in memory -- every lane fences its own
 // stores (store_env spreads them over lanes), then lane 0 publishes the epoch
@@ -2838,7 +2913,7 @@ __device__ __forceinline__ void state_ready(const Grp_& g, const LeanSched& ls, 
   if (g.lane == 0) *(volatile unsigned int*)(ls.flags + i) = ls.epoch;
 }
 
-template <int NC, bool ONE_WAVE, int FW, int FH, int G, int MINB>
+template <int NC, bool ONE_WAVE, int FW, int FH, int G, int MINB, bool RES = false>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, MINB)
 lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev st,
             const __grid_constant__ StateDev so, const long long* __restrict__ actions,
@@ -2874,12 +2949,14 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   // mapped host path: the host wrote the actions before the launch (see
   // batch_kernel); device actions are read after griddepcontrol.wait
   long long act = 0, act_next = 0;
-  if (ls.early && i < n) act = actions[i];
+  const bool gated = ls.gate_dev != nullptr;
+  if (ls.early && !gated && i < n) act = actions[i];
   // multi-wave mapped: the next ticket's action is read from host memory one
   // env ahead (after this env's dynamics), so its bus round trip overlaps
   // the render instead of stalling the warp at the top of every env
   const auto prefetch = [&](long long tn) {
-    if (!ONE_WAVE && ls.early && lane == 0 && tn < n) act_next = actions[tn];
+    if (!ONE_WAVE && ls.early && lane == 0 && tn < n)
+      act_next = gated ? ld_sys(actions + tn) : actions[tn];
   };
   stage_map_issue(S, smap, cell, solid);
   stage_map_wait();
@@ -2888,6 +2965,12 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
 #endif
   const bool chained = ls.flags != nullptr && ls.need_ready != 0;
   if (!chained) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (gated) {
+    // pipelined host step: wait here (previous grid done, tables staged)
+    // for the host to release or cancel this launch
+    if (!gate_pass(ls, ls.gate_q)) return;
+    if (ls.early && i < n) act = ld_sys(actions + i);
+  }
 #if TC_TRACE
   if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
 #endif
@@ -2898,136 +2981,149 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   // cull reads it after the dynamics): a register there would be spilled
   int* agoal_s = reinterpret_cast<int*>(rew_s + 2 * PER_CTA);
   static_assert(20 * PER_CTA <= CTA_SCRATCH, "CTA scratch: rewards, dones, goals");
-  // one wave, mapped: warps without an env still take part in the CTA's
-  // result hand-off barrier
-  if (ONE_WAVE && out.res_host && i >= n)
-    ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
-  constexpr size_t FB = (size_t)FW * FH * 3;
-  const size_t frame_bytes = FB ? FB : (size_t)S.obs_h * S.obs_w * 3;
-  bool first = true;
-  if (ONE_WAVE && chained && i < n) {
-    // this env's state from the previous step, and (need_done) the output
-    // block this launch overwrites finished by the step that last wrote it
-    if (lane == 0) {
-      const volatile unsigned int* rd = ls.flags + i;
-      const volatile unsigned int* dn = ls.flags + n + blockIdx.x;
-      while ((int)(*rd - ls.need_ready) < 0 ||
-             (ls.need_done != 0 && (int)(*dn - ls.need_done) < 0))
-        __nanosleep(64);
-    }
-    gr.sync();
-    __threadfence();  // acquire: the flag's writer fenced before setting it
-  }
-  while (i < n) {
-    long long tnext = 0;
-    if (!ONE_WAVE && lane == 0 && (counters || ls.flags))
-      tnext = ls.stride + (long long)atomicAdd(ls.flags ? ls.tickets : &counters->next_env, 1u);
-    if (!ONE_WAVE && chained) {
-      // multi-wave chained: env i's previous step (state and frames) is done
+  for (unsigned int k = 0;; k++) {
+    const StateDev& sti = (RES && (k & 1u)) ? so : st;
+    const StateDev& sto = (RES && (k & 1u)) ? st : so;
+    const OutDev& ob = (RES && (k & 1u)) ? ls.out2 : out;
+    // one wave, mapped: warps without an env still take part in the CTA's
+    // result hand-off barrier
+    if (ONE_WAVE && ob.res_host && i >= n)
+      ship_results(ob, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
+    constexpr size_t FB = (size_t)FW * FH * 3;
+    const size_t frame_bytes = FB ? FB : (size_t)S.obs_h * S.obs_w * 3;
+    bool first = true;
+    if (ONE_WAVE && chained && i < n) {
+      // this env's state from the previous step, and (need_done) the output
+      // block this launch overwrites finished by the step that last wrote it
       if (lane == 0) {
         const volatile unsigned int* rd = ls.flags + i;
-        while ((int)(*rd - ls.need_ready) < 0) __nanosleep(64);
+        const volatile unsigned int* dn = ls.flags + n + blockIdx.x;
+        while ((int)(*rd - ls.need_ready) < 0 ||
+               (ls.need_done != 0 && (int)(*dn - ls.need_done) < 0))
+          __nanosleep(64);
       }
       gr.sync();
-      __threadfence();
+      __threadfence();  // acquire: the flag's writer fenced before setting it
     }
-    if (!ls.early) {
-      act = actions[i];
-    } else if (!first) {
-      act = gr.shfl(act_next, 0);
-    }
-    first = false;
-    Env e;
-    TRACE(i, 0);
-    load_env<G>(S, st, i, e);
-    // outputs, status and host results are written as soon as they are
-    // known, so nothing but the env index stays live across the render
-    if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
-      store_env<G>(S, so, i, e);  // out-of-place: carry the state over
-      if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
-      if (lane == 0) {
-        out.statuses[i] = TC_ST_BAD_ACTION;
-        if (out.flag_host) {
-          *(volatile int32_t*)out.flag_host = 1;
-        } else if (counters) {
-          atomicOr(&counters->bad_status, 1u << TC_ST_BAD_ACTION);
+    while (i < n) {
+      long long tnext = 0;
+      if (!ONE_WAVE && lane == 0 && (counters || ls.flags))
+        tnext = ls.stride + (long long)atomicAdd(ls.flags ? ls.tickets : &counters->next_env, 1u);
+      if (!ONE_WAVE && chained) {
+        // multi-wave chained: env i's previous step (state and frames) is done
+        if (lane == 0) {
+          const volatile unsigned int* rd = ls.flags + i;
+          while ((int)(*rd - ls.need_ready) < 0) __nanosleep(64);
         }
-        if (ONE_WAVE && out.res_host) {  // a voided env reports reward 0, done 0
-          rew_s[grp] = 0.0;
-          done_s[grp] = 0;
-        }
+        gr.sync();
+        __threadfence();
       }
-      if (ONE_WAVE && out.res_host)
-        ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
-      prefetch(tnext);
-    } else {
-      TRACE(i, 1);
-      const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
-      prefetch(tnext);
-      if (lane == 0) {
-        out.rewards[i] = o.reward;
-        out.dones[i] = (uint8_t)o.done;
-        out.truncs[i] = (uint8_t)o.trunc;
-        out.events[i] = o.events;
-        out.statuses[i] = TC_ST_OK;
-        if (o.violation && counters)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&counters->violations), 1ull);
-        if (ONE_WAVE && out.res_host) {
-          // this env's [reward | done] straight to pinned host memory (the
-          // CTA's envs are contiguous: the warps' stores merge on the bus)
-          rew_s[grp] = o.reward;
-          done_s[grp] = (uint8_t)o.done;
-        }
+      if (!ls.early) {
+        act = actions[i];
+      } else if (!first) {
+        act = gr.shfl(act_next, 0);
       }
-      if (ONE_WAVE && out.res_host)
-        ship_results(out, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
-      if (o.done && auto_reset) reset_draws(S, e);
-      store_env<G>(S, so, i, e);
-      if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
-      if (lane == 0) agoal_s[grp] = e.agoal;
-      TRACE(i, 2);
-      uint8_t* frame = out.frames + (size_t)i * frame_bytes;
-      const double planex = -e.dy * PLANE_HALF_WIDTH;
-      const double planey = e.dx * PLANE_HALF_WIDTH;
-      const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h &&
-                          (e.dx != 0.0 || e.dy != 0.0);
-      int status;
-      if (inside) {
-        wall_pass<NC, false, G, true, FW, FH>(S, cell, solid, sm, e, planex, planey, nullptr,
-                                              nullptr, TC_TRACE ? i : -1);
-        status = TC_ST_OK;
+      first = false;
+      Env e;
+      TRACE(i, 0);
+      load_env<G>(S, sti, i, e);
+      // outputs, status and host results are written as soon as they are
+      // known, so nothing but the env index stays live across the render
+      if (act < 0 || act >= A_COUNT || !((S.legal_mask >> act) & 1u)) {
+        store_env<G>(S, sto, i, e);  // out-of-place: carry the state over
+        if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
+        if (lane == 0) {
+          ob.statuses[i] = TC_ST_BAD_ACTION;
+          if (ob.flag_host) {
+            *(volatile int32_t*)ob.flag_host = 1;
+          } else if (counters) {
+            atomicOr(&counters->bad_status, 1u << TC_ST_BAD_ACTION);
+          }
+          if (ONE_WAVE && ob.res_host) {  // a voided env reports reward 0, done 0
+            rew_s[grp] = 0.0;
+            done_s[grp] = 0;
+          }
+        }
+        if (ONE_WAVE && ob.res_host)
+          ship_results(ob, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
+        prefetch(tnext);
       } else {
-        status = wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, nullptr, nullptr,
-                                       false);
+        TRACE(i, 1);
+        const StepOut o = step_dynamics<G>(S, cell, solid, e, (int)act, validate);
+        prefetch(tnext);
+        if (lane == 0) {
+          ob.rewards[i] = o.reward;
+          ob.dones[i] = (uint8_t)o.done;
+          ob.truncs[i] = (uint8_t)o.trunc;
+          ob.events[i] = o.events;
+          ob.statuses[i] = TC_ST_OK;
+          if (o.violation && counters)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&counters->violations), 1ull);
+          if (ONE_WAVE && ob.res_host) {
+            // this env's [reward | done] straight to pinned host memory (the
+            // CTA's envs are contiguous: the warps' stores merge on the bus)
+            rew_s[grp] = o.reward;
+            done_s[grp] = (uint8_t)o.done;
+          }
+        }
+        if (ONE_WAVE && ob.res_host)
+          ship_results(ob, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
+        if (o.done && auto_reset) reset_draws(S, e);
+        store_env<G>(S, sto, i, e);
+        if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
+        if (lane == 0) agoal_s[grp] = e.agoal;
+        TRACE(i, 2);
+        uint8_t* frame = ob.frames + (size_t)i * frame_bytes;
+        const double planex = -e.dy * PLANE_HALF_WIDTH;
+        const double planey = e.dx * PLANE_HALF_WIDTH;
+        const bool inside = e.x >= 0.0 && e.y >= 0.0 && e.x < (double)S.w && e.y < (double)S.h &&
+                            (e.dx != 0.0 || e.dy != 0.0);
+        int status;
+        if (inside) {
+          wall_pass<NC, false, G, true, FW, FH>(S, cell, solid, sm, e, planex, planey, nullptr,
+                                                nullptr, TC_TRACE ? i : -1);
+          status = TC_ST_OK;
+        } else {
+          status = wall_pass_cold<NC, G>(S, cell, solid, sm, e, planex, planey, nullptr, nullptr,
+                                         false);
+        }
+        gr.sync();
+        TRACE(i, 3);
+        if (status == TC_ST_OK) {
+          e.agoal = agoal_s[grp];  // (the wall pass synced the group)
+          const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
+          TRACE(i, 4);
+  #if TC_TRACE
+          if (g_trace && lane == 0) g_trace[i * 16 + 7] = (unsigned long long)m;
+  #endif
+          if constexpr (FW != 0) mirror_contig_fixed<FW, FH, G>(S, sm, m, frame);
+          else mirror_contig<NC, G>(S, sm, m, frame);
+        } else if (lane == 0) {
+          ob.statuses[i] = status;
+          if (counters) atomicOr(&counters->bad_status, 1u << status);
+        }
       }
-      gr.sync();
-      TRACE(i, 3);
-      if (status == TC_ST_OK) {
-        e.agoal = agoal_s[grp];  // (the wall pass synced the group)
-        const int m = S.n_ent ? sprite_setup<G>(S, sm, e, planex, planey, nullptr) : 0;
-        TRACE(i, 4);
-#if TC_TRACE
-        if (g_trace && lane == 0) g_trace[i * 16 + 7] = (unsigned long long)m;
-#endif
-        if constexpr (FW != 0) mirror_contig_fixed<FW, FH, G>(S, sm, m, frame);
-        else mirror_contig<NC, G>(S, sm, m, frame);
-      } else if (lane == 0) {
-        out.statuses[i] = status;
-        if (counters) atomicOr(&counters->bad_status, 1u << status);
+  #if TC_TRACE
+      if (g_trace && lane == 0) {
+        unsigned int smid;
+        asm("mov.u32 %0, %smid;" : "=r"(smid));
+        g_trace[i * 16 + 5] = gtime();
+        g_trace[i * 16 + 6] = smid | ((unsigned long long)grp << 16) |
+                             ((unsigned long long)blockIdx.x << 32);
       }
+  #endif
+      if (ONE_WAVE) break;
+      if (ls.flags) state_ready(gr, ls, i);  // multi-wave chained: the whole step
+      i = (counters || ls.flags) ? gr.shfl(tnext, 0) : i + ls.stride;
     }
-#if TC_TRACE
-    if (g_trace && lane == 0) {
-      unsigned int smid;
-      asm("mov.u32 %0, %smid;" : "=r"(smid));
-      g_trace[i * 16 + 5] = gtime();
-      g_trace[i * 16 + 6] = smid | ((unsigned long long)grp << 16) |
-                           ((unsigned long long)blockIdx.x << 32);
+    if constexpr (!RES) {
+      break;
+    } else {
+      // resident host-step loop: step k + 1 of the ping-pong, once the host
+      // has written its actions (or the end of the loop: a cancel)
+      if (!gate_pass(ls, ls.gate_q + k + 1u)) return;
+      if (i < n) act = ld_sys(actions + i);
     }
-#endif
-    if (ONE_WAVE) break;
-    if (ls.flags) state_ready(gr, ls, i);  // multi-wave chained: the whole step
-    i = (counters || ls.flags) ? gr.shfl(tnext, 0) : i + ls.stride;
   }
 #if TC_TRACE
   if (g_trace_cta) {
@@ -3743,19 +3839,141 @@ int tc_spec_destroy(tc_spec* s) {
   return e == cudaSuccess ? TC_OK : cuda_fail(e, "cudaFree(spec)");
 }
 
+// ---------------------------------------------- pipelined host step state
+// tc_batch_step_pipelined launches step s+1 right after releasing step s,
+// before the host knows step s+1's actions: the launch stages its tables,
+// waits for step s's grid, then waits at a gate (LeanSched::gate_*). The
+// next call with the matching arguments releases it with one host store
+// instead of launching, so the launch call, the launch latency and the
+// previous step's frame rendering are off the host's critical path. At most
+// one such launch is pending per process; any other library launch cancels
+// it first, and a watchdog thread cancels it if no call releases it within
+// the timeout (TILECAST_PIPE_TIMEOUT_US, default 1000), so other work on the
+// stream or the GPU is never held longer than that. After a timeout the
+// pipeline backs off (exponentially, up to 4096 steps without speculation).
+namespace {
+struct PipeKey {
+  const tc_spec* spec;
+  tc_state in, out;  // pointer-only structs: compared bytewise
+  tc_out ob;
+  int64_t n;
+  int32_t auto_reset, validate;
+  tc_counters* counters;
+  const int64_t* acts;
+  uint8_t* res;
+  int32_t* flag;
+  void* stream;
+};
+PipeKey pipe_key(const tc_mapped_call& m, const tc_state* in, const tc_state* out,
+                 const tc_out* ob) {
+  PipeKey k;
+  memset(&k, 0, sizeof(k));
+  k.spec = m.spec; k.in = *in; k.out = *out; k.ob = *ob; k.n = m.n;
+  k.auto_reset = m.auto_reset; k.validate = m.validate; k.counters = m.counters_dev;
+  k.acts = m.actions_host; k.res = m.results_host; k.flag = m.flag_host; k.stream = m.stream;
+  return k;
+}
+bool same_key(const PipeKey& a, const PipeKey& b) { return memcmp(&a, &b, sizeof(PipeKey)) == 0; }
+
+struct Pipe {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::atomic<bool> pending{false};
+  PipeKey key;
+  unsigned int q = 0;  // last gate number issued (host words hold the last go / cancel)
+  double t_launch = 0.0, timeout_us = 1000.0;
+  int skip = 0, backoff = 0;
+  bool watchdog = false, idle = false;
+  bool resident = false;  // the pending gate belongs to a resident loop kernel
+  unsigned long long released = 0, cancelled = 0, timeouts = 0;
+};
+Pipe& pipe() {  // never destroyed: the watchdog thread may outlive static destruction
+  static Pipe* p = [] {
+    Pipe* x = new Pipe();
+    const char* e = getenv("TILECAST_PIPE_TIMEOUT_US");
+    if (e && atof(e) > 0) x->timeout_us = atof(e);
+    return x;
+  }();
+  return *p;
+}
+// the cancel store (mu held): the gated kernel exits without any effect
+void pipe_cancel_locked(Pipe& P, bool timeout) {
+  if (!P.pending.load(std::memory_order_relaxed)) return;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *reinterpret_cast<volatile uint32_t*>(P.key.flag + 5) = P.q;
+  P.pending.store(false, std::memory_order_release);
+  P.resident = false;
+  P.cancelled++;
+  if (timeout) {
+    P.timeouts++;
+    P.backoff = P.backoff ? std::min(2 * P.backoff, 4096) : 8;
+    P.skip = P.backoff;
+  }
+}
+void pipe_watchdog() {
+  Pipe& P = pipe();
+  std::unique_lock<std::mutex> lk(P.mu);
+  for (;;) {
+    if (!P.pending.load(std::memory_order_relaxed)) {
+      P.idle = true;
+      P.cv.wait(lk);
+      P.idle = false;
+      continue;
+    }
+    const double left = P.t_launch + P.timeout_us - host_us();
+    if (left <= 0.0) {
+      pipe_cancel_locked(P, true);
+      continue;
+    }
+    P.cv.wait_for(lk, std::chrono::microseconds((long long)left + 1));
+  }
+}
+}  // namespace
+
+// TILECAST_PIPE_RESIDENT=0: one gated launch per pipelined step always
+const bool g_pipe_resident = [] {
+  const char* e = getenv("TILECAST_PIPE_RESIDENT");
+  return e ? atoi(e) != 0 : true;
+}();
+
+static void pipe_cancel_if_pending() {
+  Pipe& P = pipe();
+  if (!P.pending.load(std::memory_order_acquire)) return;
+  std::lock_guard<std::mutex> lk(P.mu);
+  pipe_cancel_locked(P, false);
+}
+
 struct ChainArgs {
   unsigned int* flags;
   unsigned int* tickets;  // multi-wave: this launch's zeroed ticket counter
   unsigned int epoch, need_ready, need_done;
 };
 
+struct GateArgs {  // a pipelined (gated) launch, LeanSched::gate_*
+  unsigned int* dev;
+  const unsigned long long* host;
+  unsigned int q;
+  const tc_out* out2;  // non-NULL: the resident host-step loop (RES kernel)
+};
+
+// the resident host-step loop kernel for a one-wave batch of this spec, or
+// NULL (then the pipeline launches one gated kernel per step)
+static const void* select_resident(const tc_spec* s) {
+  if (s->dev.obs_w == 64 && s->dev.obs_h == 64)
+    return (const void*)lean_kernel<2, true, 64, 64, 32, TC_MIN_CTAS_LEAN, true>;
+  return nullptr;
+}
+
 static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc_state* state_out,
                                const int64_t* actions_dev, const tc_out* out, int64_t n,
                                int32_t mode, int32_t auto_reset, int32_t validate,
                                tc_counters* counters_dev, void* stream,
                                uint8_t* res_host = nullptr, int32_t* flag_host = nullptr,
-                               const ChainArgs* chain = nullptr) {
+                               const ChainArgs* chain = nullptr, const GateArgs* gate = nullptr) {
   if (!s || !state || !out) return fail(TC_E_INVALID, "NULL spec/state/out");
+  // any other launch first cancels a pipelined step still waiting for its
+  // actions (it would hold every SM until the watchdog cancelled it)
+  if (!gate) pipe_cancel_if_pending();
   if (n < 0) return fail(TC_E_INVALID, "n must be >= 0");
   if (mode != TC_MODE_RESET && mode != TC_MODE_STEP && mode != MODE_RENDER)
     return fail(TC_E_INVALID, "mode must be 0 (reset) or 1 (step)");
@@ -3796,6 +4014,14 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     ls.ctas = one_wave ? (int)((n + ls.epc - 1) / ls.epc) : 0;
     ls.flags = ls.tickets = nullptr;
     ls.epoch = ls.need_ready = ls.need_done = 0;
+    ls.gate_dev = gate ? gate->dev : nullptr;
+    ls.gate_host = gate ? gate->host : nullptr;
+    ls.gate_q = gate ? gate->q : 0u;
+    ls.out2 = (gate && gate->out2) ? to_dev(gate->out2) : od;
+    if (gate && gate->out2) {
+      ls.out2.res_host = res_host;
+      ls.out2.flag_host = flag_host;
+    }
     if (chain && !res_host) {
       ls.flags = chain->flags;
       ls.tickets = chain->tickets;
@@ -3817,7 +4043,9 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TC_CUDA(cudaLaunchKernelExC(&cfg, select_lean(d.obs_w, d.obs_h, one_wave), args));
+    const void* fn = (gate && gate->out2) ? select_resident(s) : select_lean(d.obs_w, d.obs_h, one_wave);
+    if (!fn) return fail(TC_E_INVALID, "no resident kernel for this frame shape");
+    TC_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
     return TC_OK;
   }
   const bool wide = taps || use_wide(s, n);
@@ -4001,6 +4229,7 @@ int tc_multi_step(const tc_spec* const* specs, const tc_state* states_in,
                   const tc_state* states_out, const int64_t* actions_dev, const tc_out* outs,
                   const int64_t* counts, int32_t n_groups, int32_t auto_reset, int32_t validate,
                   tc_counters* const* counters, void* stream) {
+  pipe_cancel_if_pending();
   if (!specs || !states_in || !states_out || !actions_dev || !outs || !counts || !counters)
     return fail(TC_E_INVALID, "NULL group array");
   if (n_groups < 1) return fail(TC_E_INVALID, "n_groups must be >= 1");
@@ -4174,6 +4403,135 @@ int tc_batch_step_mapped_call(const tc_mapped_call* c) {
                               c->flag_host, c->stream);
 }
 
+int tc_batch_step_pipelined(const tc_pipe_call* c) {
+  if (!c) return fail(TC_E_INVALID, "NULL call");
+  const tc_mapped_call& m = c->step;
+  if (!m.actions_host || !m.results_host || !m.flag_host || !m.counters_dev)
+    return fail(TC_E_INVALID, "NULL actions / results / flag / counters");
+  if (!m.spec || !m.state_in || !m.state_out || !m.out)
+    return fail(TC_E_INVALID, "NULL spec / state / out");
+  if (m.n <= 0) return m.n == 0 ? TC_OK : fail(TC_E_INVALID, "n must be >= 0");
+  if (reinterpret_cast<uint8_t*>(m.out->rewards) + (size_t)m.n * 8 != m.out->dones)
+    return fail(TC_E_INVALID, "out->dones must follow out->rewards ([rewards | dones])");
+  if ((reinterpret_cast<uintptr_t>(m.out->rewards) | reinterpret_cast<uintptr_t>(m.results_host) |
+       reinterpret_cast<uintptr_t>(m.flag_host)) & 15u)
+    return fail(TC_E_INVALID, "rewards / results_host / flag_host must be 16-byte aligned");
+  Pipe& P = pipe();
+  std::unique_lock<std::mutex> lk(P.mu);
+  volatile int32_t* done = m.flag_host + 1;
+  bool released = false;
+  if (P.pending.load(std::memory_order_relaxed)) {
+    if (same_key(P.key, pipe_key(m, m.state_in, m.state_out, m.out))) {
+      // this step is already resident behind its gate: open it. The host's
+      // earlier stores (actions, the flag words) are ordered before the go
+      // word (x86 TSO; the fence keeps the compiler from reordering them)
+      *done = 0;
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      *reinterpret_cast<volatile uint32_t*>(m.flag_host + 4) = P.q;
+      P.pending.store(false, std::memory_order_release);
+      P.released++;
+      P.backoff = 0;
+      released = true;
+      if (P.resident) {
+        // the resident loop goes on to the next step of the ping-pong: it
+        // is pending again (gate q + 1) without a launch
+        P.q++;
+        P.key = pipe_key(m, m.state_out, m.state_in, c->next_out);
+        P.t_launch = host_us();
+        P.pending.store(true, std::memory_order_release);
+      }
+    } else {
+      pipe_cancel_locked(P, false);
+    }
+  }
+  if (!released) {
+    // the first step of a run (or after a cancel): an ordinary mapped launch
+    if (tc_batch_step_mapped(m.spec, m.state_in, m.state_out, m.actions_host, m.out, m.n,
+                             m.auto_reset, m.validate, m.counters_dev, m.results_host,
+                             m.flag_host, m.stream) != TC_OK)
+      return TC_E_CUDA;
+    // (tc_batch_step_mapped waited for the results: nothing left to wait for
+    // but the successor's launch below)
+  }
+  // the successor (reuse=True ping-pong: this step's out state is its input,
+  // this step's input block its output state, c->next_out its output block)
+  const bool taps = c->next_out && (c->next_out->zbuf || c->next_out->rayinfo ||
+                                    c->next_out->spritevis);
+  const int lkind = lean_kind(m.spec, m.n);
+  if (c->speculate && c->next_out && c->gate_dev && !taps && lkind != 0 &&
+      !P.pending.load(std::memory_order_relaxed)) {
+    if (P.skip > 0) {
+      P.skip--;
+    } else {
+      if (++P.q == 0) ++P.q;
+      // one-wave 64x64 batches: a resident loop kernel (stays on the GPU
+      // across steps); otherwise one gated launch per step
+      const bool res = g_pipe_resident && lkind == 1 && select_resident(m.spec) != nullptr;
+      GateArgs g{c->gate_dev, reinterpret_cast<const unsigned long long*>(m.flag_host + 4), P.q,
+                 res ? m.out : nullptr};
+      const int rc = launch_batch_kernel(m.spec, m.state_out, m.state_in, m.actions_host,
+                                         c->next_out, m.n, TC_MODE_STEP, m.auto_reset,
+                                         m.validate, m.counters_dev, m.stream, m.results_host,
+                                         m.flag_host, nullptr, &g);
+      if (rc != TC_OK) return rc;
+      P.key = pipe_key(m, m.state_out, m.state_in, c->next_out);
+      P.t_launch = host_us();
+      P.resident = res;
+      P.pending.store(true, std::memory_order_release);
+      if (!P.watchdog) {
+        std::thread(pipe_watchdog).detach();
+        P.watchdog = true;
+      } else if (P.idle) {
+        P.cv.notify_one();
+      }
+    }
+  }
+  lk.unlock();
+  if (!released) return TC_OK;
+  // wait for the released step's results (as tc_batch_step_mapped): the
+  // stream now also holds the successor, so a step that ended without
+  // results surfaces once the successor is released or cancelled
+  for (unsigned spin = 1; *done == 0; spin++) {
+    if ((spin & 1023u) == 0) {
+      const cudaError_t q = cudaStreamQuery((cudaStream_t)m.stream);
+      if (q == cudaSuccess) {
+        if (*done == 0) return fail(TC_E_CUDA, "step kernel finished without results");
+        break;
+      }
+      if (q != cudaErrorNotReady) {
+        cudaGetLastError();
+        return fail(TC_E_CUDA, cudaGetErrorString(q));
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  return TC_OK;
+}
+
+int tc_pipe_cancel(void) {
+  pipe_cancel_if_pending();
+  return TC_OK;
+}
+
+int tc_pipe_reset(void) {
+  Pipe& P = pipe();
+  std::lock_guard<std::mutex> lk(P.mu);
+  pipe_cancel_locked(P, false);
+  P.skip = P.backoff = 0;
+  return TC_OK;
+}
+
+int tc_pipe_stats(uint64_t* out4) {
+  if (!out4) return fail(TC_E_INVALID, "NULL out");
+  Pipe& P = pipe();
+  std::lock_guard<std::mutex> lk(P.mu);
+  out4[0] = P.released;
+  out4[1] = P.cancelled;
+  out4[2] = P.timeouts;
+  out4[3] = P.pending.load() ? 1u : 0u;
+  return TC_OK;
+}
+
 // perf diagnostics of the mapped host step: mean host microseconds in the
 // launch call and in the wait for the completion word since the last reset
 int tc_debug_mapped_timing(double* out3, int32_t reset) {
@@ -4190,6 +4548,7 @@ int tc_debug_mapped_timing(double* out3, int32_t reset) {
 int tc_rollout(const tc_spec* s, const tc_state* state, const tc_out* out, int64_t n,
                int64_t base, int64_t n_total, uint64_t policy_key, int64_t step0,
                int32_t k_steps, int32_t frame_ring, tc_counters* counters_dev, void* stream) {
+  pipe_cancel_if_pending();
   if (!s || !state || !out || !out->frames) return fail(TC_E_INVALID, "NULL spec/state/out");
   if (n < 0 || k_steps < 0 || frame_ring < 1) return fail(TC_E_INVALID, "bad n/k/ring");
   if (n == 0 || k_steps == 0) return TC_OK;
