@@ -147,10 +147,15 @@ const char *tc_step_kernel(const tc_spec *spec, int64_t n);
 /* Perf diagnostics (not part of the reference contract): per-env and
  * per-CTA timestamp buffers (TC_TRACE builds only; TC_E_INVALID otherwise),
  * and the mean host-side split of tc_batch_step_mapped (launch call, wait
- * for the results, call count) since the last reset. */
+ * for the results, call count) since the last reset (reset = 2: the split
+ * of the released tc_batch_step_pipelined steps instead -- release call,
+ * wait for the results, count -- then reset). */
 int tc_debug_trace(void *dev_buf);
 int tc_debug_trace_cta(void *dev_buf);
 int tc_debug_mapped_timing(double *out3, int32_t reset);
+/* The resident pipelined loop's device timeline (TILECAST_PIPE_TRACE=1):
+ * u64 globaltimer [64 steps][3 stamps][grid CTAs], *grid = CTAs. */
+int tc_debug_pipe_trace(uint64_t *host, int64_t cap, int32_t *grid);
 
 /* Pack + upload a spec's tables once (replaces build_tables' device half,
  * tables.py:92-184). `host` points at host arrays. */
@@ -277,8 +282,9 @@ int tc_batch_step_mapped_call(const tc_mapped_call *call);
  * this step's frame rendering leave the host's per-step critical path.
  * flag_host is int32[8] (16-byte aligned): [0] bad action, [1] results
  * ready (as tc_batch_step_mapped), [4] / [5] the gate's go / cancel words,
- * [6] expired mark -- all managed by the call except [0]. gate_dev is one
- * zeroed device uint32 per action stage. A call that does not match the
+ * [6] expired mark -- all managed by the call except [0]. gate_dev is a
+ * zeroed device uint32[4096] per action stage (the gate's broadcast lines and
+ * the result hand-off counters). A call that does not match the
  * pending launch (other buffers, another batch) cancels it first, as does
  * every other library launch; a watchdog thread cancels a launch nobody
  * released within TILECAST_PIPE_TIMEOUT_US (default 1000 us), so work queued
@@ -289,9 +295,9 @@ int tc_batch_step_mapped_call(const tc_mapped_call *call);
 typedef struct tc_pipe_call {
   tc_mapped_call step;
   const tc_out *next_out;
-  uint32_t *gate_dev;
+  uint32_t *gate_dev;   /* zeroed device uint32[4096] per action stage */
   int32_t speculate;
-  int32_t pad;
+  int32_t device;       /* the CUDA device of the batch (made current for the call) */
 } tc_pipe_call;
 int tc_batch_step_pipelined(const tc_pipe_call *call);
 /* Cancel a pending pipelined launch (no-op if none). */

@@ -63,7 +63,7 @@ class TcMappedCall(C.Structure):
 class TcPipeCall(C.Structure):
     """tc_pipe_call: a mapped step plus the successor's output block and gate."""
     _fields_ = [("step", TcMappedCall), ("next_out", _p), ("gate_dev", _p),
-                ("speculate", C.c_int32), ("pad", C.c_int32)]
+                ("speculate", C.c_int32), ("device", C.c_int32)]
 
 
 class NativeError(RuntimeError):
@@ -116,6 +116,8 @@ def _load() -> C.CDLL:
         "tc_pipe_cancel": (C.c_int, []),
         "tc_pipe_reset": (C.c_int, []),
         "tc_pipe_stats": (C.c_int, [_p]),
+        "tc_debug_mapped_timing": (C.c_int, [_p, C.c_int32]),
+        "tc_debug_pipe_trace": (C.c_int, [_p, C.c_int64, _p]),
         "tc_rollout": (C.c_int, [_p, P(TcState), P(TcOut), C.c_int64, C.c_int64, C.c_int64,
                                  C.c_uint64, C.c_int64, C.c_int32, C.c_int32, _p, _p]),
         "tc_seed_streams": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, _p, _p, _p]),

@@ -141,7 +141,8 @@ class _ActionStage:
         # [0] bad action, [1] results ready, [4] / [5] pipelined gate go /
         # cancel, [6] expired (tc_batch_step_pipelined)
         self._h_flag = torch.zeros(8, dtype=torch.int32, pin_memory=True)
-        self.gate_dev = torch.zeros(1, dtype=torch.int32, device=device)
+        # the pipelined step's gate lines and result hand-off counters
+        self.gate_dev = torch.zeros(4096, dtype=torch.int32, device=device)
         self.h_flag = self._h_flag.numpy()
         self.h_flag_ptr = self._h_flag.data_ptr()
         self.h_act_ptr = self._h_act.data_ptr()
@@ -332,18 +333,15 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
                                          N.C.addressof(so), stg.h_act_ptr, N.C.addressof(oc),
                                          bs.n, 1, 1 if validate else 0, N.ptr(bs._counters),
                                          stg.h_rew_ptr, stg.h_flag_ptr, stream_ptr(bs.device)),
-                          N.C.addressof(nc), stg.gate_dev.data_ptr(), 1 if spec_next else 0, 0)
+                          N.C.addressof(nc), stg.gate_dev.data_ptr(), 1 if spec_next else 0,
+                          stg.dev_index)
         if len(stg.calls) > 8:
             stg.calls.clear()
         # keep the structs and blocks alive with the key
         stg.calls[key] = call = (N.C.addressof(cs), cs, si, so, oc, nc, bs._sb, sb, ob, bs._ob)
     if stg.fn is None:
         stg.fn = N.lib().tc_batch_step_pipelined
-    if torch.cuda.current_device() == stg.dev_index:
-        rc = stg.fn(call[0])
-    else:
-        with torch.cuda.device(bs.device):
-            rc = stg.fn(call[0])
+    rc = stg.fn(call[0])  # (the call makes the batch's device current itself)
     if rc:
         N.check(rc, "tc_batch_step_mapped")
     if stg.h_flag[0]:

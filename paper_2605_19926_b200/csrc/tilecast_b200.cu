@@ -2845,7 +2845,13 @@ struct LeanSched {
   // instead of exiting; a cancel ends it with every state block as an
   // ordinary launch sequence would have left it
   OutDev out2;
+  // resident loop timeline (TILECAST_PIPE_TRACE=1 only): globaltimer per
+  // step k < 64 and CTA: [k][0] past the gate, [k][1] results shipped,
+  // [k][2] frame written
+  unsigned long long* rtrace;
 };
+
+constexpr int GATE_LINES = 32;  // gate_dev: GATE_LINES words, 128 B apart
 
 // the pipelined step's gate (see LeanSched): true = released (the host's
 // actions for this step are in pinned memory), false = cancelled. A launch
@@ -2864,6 +2870,22 @@ __device__ __forceinline__ unsigned long long gate_clock() {
 // the host's actions. (A relaxed.sys load per warp instead costs ~140 us per
 // step at 4096 envs, measured: sys-scope loads of pinned memory serialise.)
 __device__ __forceinline__ long long ld_sys(const long long* p) { return *p; }
+__device__ __forceinline__ void rstamp(const LeanSched& ls, unsigned int k, int slot) {
+  if (ls.rtrace && threadIdx.x == 0 && k < 64u)
+    ls.rtrace[((size_t)k * 3 + slot) * gridDim.x + blockIdx.x] = gate_clock();
+}
+// the actions after the gate: one wave, the CTA's contiguous run in one bus
+// read (4,096 single-env reads of pinned memory queue on the bus: +2 us per
+// step), parked in the CTA scratch; multi-wave, per env
+template <bool ONE_WAVE>
+__device__ __forceinline__ long long gate_actions(const LeanSched& ls, const long long* actions,
+                                                  long long i, long long cbase, int cta_envs,
+                                                  long long* act_s) {
+  if (!ONE_WAVE) return i < ls.n ? ld_sys(actions + i) : 0;
+  if (threadIdx.x < (unsigned)cta_envs) act_s[threadIdx.x] = ld_sys(actions + cbase + threadIdx.x);
+  __syncthreads();
+  return i < ls.n ? act_s[threadIdx.x >> 5] : 0;
+}
 __device__ __noinline__ bool gate_pass(const LeanSched& ls, unsigned int q) {
   bool go = false;
   if (threadIdx.x == 0) {
@@ -2873,11 +2895,7 @@ __device__ __noinline__ bool gate_pass(const LeanSched& ls, unsigned int q) {
       const unsigned long long t0 = gate_clock();
       for (unsigned int spin = 0;; spin++) {
         unsigned long long hw;
-#if TC_GATE_POLL == 1
-        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(hw) : "l"(ls.gate_host) : "memory");
-#else
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(hw) : "l"(ls.gate_host) : "memory");
-#endif
         if ((unsigned int)hw == q) { w = q2; break; }
         if ((unsigned int)(hw >> 32) == q) { w = q2 + 1u; break; }
         if ((spin & 255u) == 255u && gate_clock() - t0 > 1000000000ull) {
@@ -2886,18 +2904,21 @@ __device__ __noinline__ bool gate_pass(const LeanSched& ls, unsigned int q) {
           __threadfence_system();
           break;
         }
-        __nanosleep(64);
       }
-#if TC_GATE_POLL == 1
-      __threadfence_system();  // fence-based acquire of the host's stores
-#endif
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ls.gate_dev), "r"(w) : "memory");
+      // publish to GATE_LINES copies (one 128-byte line each) so the other
+      // CTAs' polls spread over lines instead of queueing on one: a
+      // fence-based release, then relaxed stores
+      __threadfence();
+#pragma unroll 1
+      for (int l = 0; l < GATE_LINES; l++)
+        asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(ls.gate_dev + l * 32), "r"(w) : "memory");
     } else {
+      const unsigned int* line = ls.gate_dev + (blockIdx.x % GATE_LINES) * 32;
       for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(w) : "l"(ls.gate_dev) : "memory");
+        asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(w) : "l"(line) : "memory");
         if ((int)(w - q2) >= 0) break;
-        __nanosleep(100);
       }
+      __threadfence();  // fence-based acquire
     }
     go = w == q2;
   }
@@ -2946,6 +2967,11 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
   long long i = ONE_WAVE ? (grp < cta_envs ? cbase + grp : n)
                          : (long long)grp * gridDim.x + blockIdx.x;
   const int map_bytes = map_smem_bytes(S);
+  // CTA scratch after the per-warp windows: [rewards f64 | dones u8 | goals
+  // i32 | (pipelined, one wave) actions i64 at +96]
+  long long* const act_s =
+      reinterpret_cast<long long*>(smem + map_bytes + PER_CTA * S.warp_smem + 96);
+  static_assert(!ONE_WAVE || 96 + 8 * PER_CTA <= CTA_SCRATCH, "CTA scratch: actions");
   // mapped host path: the host wrote the actions before the launch (see
   // batch_kernel); device actions are read after griddepcontrol.wait
   long long act = 0, act_next = 0;
@@ -2969,7 +2995,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     // pipelined host step: wait here (previous grid done, tables staged)
     // for the host to release or cancel this launch
     if (!gate_pass(ls, ls.gate_q)) return;
-    if (ls.early && i < n) act = ld_sys(actions + i);
+    if (ls.early) act = gate_actions<ONE_WAVE>(ls, actions, i, cbase, cta_envs, act_s);
   }
 #if TC_TRACE
   if (g_trace_cta && threadIdx.x == 0) tcta[2] = gtime();
@@ -2985,6 +3011,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     const StateDev& sti = (RES && (k & 1u)) ? so : st;
     const StateDev& sto = (RES && (k & 1u)) ? st : so;
     const OutDev& ob = (RES && (k & 1u)) ? ls.out2 : out;
+    if constexpr (RES) rstamp(ls, k, 0);
     // one wave, mapped: warps without an env still take part in the CTA's
     // result hand-off barrier
     if (ONE_WAVE && ob.res_host && i >= n)
@@ -3068,6 +3095,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
         }
         if (ONE_WAVE && ob.res_host)
           ship_results(ob, counters, n, cbase, cta_envs, ls.ctas, rew_s, done_s);
+        if constexpr (RES) rstamp(ls, k, 1);
         if (o.done && auto_reset) reset_draws(S, e);
         store_env<G>(S, sto, i, e);
         if (ONE_WAVE && ls.flags) state_ready(gr, ls, i);
@@ -3121,8 +3149,9 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     } else {
       // resident host-step loop: step k + 1 of the ping-pong, once the host
       // has written its actions (or the end of the loop: a cancel)
+      rstamp(ls, k, 2);
       if (!gate_pass(ls, ls.gate_q + k + 1u)) return;
-      if (i < n) act = ld_sys(actions + i);
+      act = gate_actions<ONE_WAVE>(ls, actions, i, cbase, cta_envs, act_s);
     }
   }
 #if TC_TRACE
@@ -3287,7 +3316,7 @@ struct tc_spec {
 namespace {
 
 thread_local std::string g_err;
-thread_local double g_mapped_time[3] = {0.0, 0.0, 0.0};
+thread_local double g_mapped_time[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 double host_us() {
   timespec ts;
   clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -3930,6 +3959,25 @@ void pipe_watchdog() {
 }
 }  // namespace
 
+// TILECAST_PIPE_TRACE=1: the resident loop records its timeline (rstamp)
+unsigned long long* g_pipe_trace = nullptr;
+int g_pipe_trace_grid = 0;
+static unsigned long long* pipe_trace_buf(int grid, void* stream) {
+  static const bool on = [] {
+    const char* e = getenv("TILECAST_PIPE_TRACE");
+    return e && atoi(e) != 0;
+  }();
+  if (!on) return nullptr;
+  if (g_pipe_trace_grid < grid) {
+    if (g_pipe_trace) cudaFree(g_pipe_trace);
+    g_pipe_trace = nullptr;
+    if (cudaMalloc(&g_pipe_trace, (size_t)64 * 3 * grid * 8) != cudaSuccess) return nullptr;
+    g_pipe_trace_grid = grid;
+  }
+  cudaMemsetAsync(g_pipe_trace, 0, (size_t)64 * 3 * grid * 8, (cudaStream_t)stream);
+  return g_pipe_trace;
+}
+
 // TILECAST_PIPE_RESIDENT=0: one gated launch per pipelined step always
 const bool g_pipe_resident = [] {
   const char* e = getenv("TILECAST_PIPE_RESIDENT");
@@ -4018,6 +4066,7 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     ls.gate_host = gate ? gate->host : nullptr;
     ls.gate_q = gate ? gate->q : 0u;
     ls.out2 = (gate && gate->out2) ? to_dev(gate->out2) : od;
+    ls.rtrace = (gate && gate->out2) ? pipe_trace_buf(grid, stream) : nullptr;
     if (gate && gate->out2) {
       ls.out2.res_host = res_host;
       ls.out2.flag_host = flag_host;
@@ -4416,6 +4465,16 @@ int tc_batch_step_pipelined(const tc_pipe_call* c) {
   if ((reinterpret_cast<uintptr_t>(m.out->rewards) | reinterpret_cast<uintptr_t>(m.results_host) |
        reinterpret_cast<uintptr_t>(m.flag_host)) & 15u)
     return fail(TC_E_INVALID, "rewards / results_host / flag_host must be 16-byte aligned");
+  const double t0 = host_us();
+  // the call's device (the struct carries it: the caller need not switch)
+  struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int want) {
+      if (cudaGetDevice(&prev) == cudaSuccess && prev != want) cudaSetDevice(want);
+      else prev = -1;
+    }
+    ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+  } dev_guard(c->device);
   Pipe& P = pipe();
   std::unique_lock<std::mutex> lk(P.mu);
   volatile int32_t* done = m.flag_host + 1;
@@ -4488,6 +4547,7 @@ int tc_batch_step_pipelined(const tc_pipe_call* c) {
   }
   lk.unlock();
   if (!released) return TC_OK;
+  const double t1 = host_us();
   // wait for the released step's results (as tc_batch_step_mapped): the
   // stream now also holds the successor, so a step that ended without
   // results surfaces once the successor is released or cancelled
@@ -4505,6 +4565,18 @@ int tc_batch_step_pipelined(const tc_pipe_call* c) {
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
+  // released steps: [3] release + bookkeeping, [4] wait for results, [5] count
+  g_mapped_time[3] += t1 - t0;
+  g_mapped_time[4] += host_us() - t1;
+  g_mapped_time[5] += 1.0;
+  return TC_OK;
+}
+
+int tc_debug_pipe_trace(uint64_t* host, int64_t cap, int32_t* grid) {
+  if (grid) *grid = g_pipe_trace_grid;
+  if (!g_pipe_trace || !host) return TC_OK;
+  const size_t nb = std::min<size_t>((size_t)cap, (size_t)64 * 3 * g_pipe_trace_grid) * 8;
+  TC_CUDA(cudaMemcpy(host, g_pipe_trace, nb, cudaMemcpyDeviceToHost));
   return TC_OK;
 }
 
@@ -4541,7 +4613,13 @@ int tc_debug_mapped_timing(double* out3, int32_t reset) {
     out3[1] = g_mapped_time[1] / k;
     out3[2] = g_mapped_time[2];
   }
-  if (reset) g_mapped_time[0] = g_mapped_time[1] = g_mapped_time[2] = 0.0;
+  if (out3 && reset == 2) {  // the pipelined released steps' split instead
+    const double k = g_mapped_time[5] > 0 ? g_mapped_time[5] : 1.0;
+    out3[0] = g_mapped_time[3] / k;
+    out3[1] = g_mapped_time[4] / k;
+    out3[2] = g_mapped_time[5];
+  }
+  if (reset) for (double& v : g_mapped_time) v = 0.0;
   return TC_OK;
 }
 

@@ -1,5 +1,7 @@
 """Per-call host time of the pipelined host step (batch_step_host, reuse=True)
 and the pipeline counters: python tools/pipe_probe.py [env] [n] [steps]."""
+import ctypes as C
+import os
 import sys
 import time
 from pathlib import Path
@@ -24,6 +26,7 @@ for pipeline in (False, True):
     tc.pipeline_drain()
     torch.cuda.synchronize()
     N.pipe_reset()
+    N.lib().tc_debug_mapped_timing(None, 1)
     s0 = N.pipe_stats()
     ts = np.zeros(K)
     t00 = time.perf_counter()
@@ -32,6 +35,8 @@ for pipeline in (False, True):
         bs, r, d = tc.batch_step_host(bs, acts[5 + s], reuse=True, pipeline=pipeline)
         ts[s] = time.perf_counter() - t0
     el = time.perf_counter() - t00
+    split = np.zeros(3)
+    N.lib().tc_debug_mapped_timing(split.ctypes.data, 2)
     tc.pipeline_drain()
     torch.cuda.synchronize()
     s1 = N.pipe_stats()
@@ -42,3 +47,25 @@ for pipeline in (False, True):
           f"released {s1['released'] - s0['released']} cancelled {s1['cancelled'] - s0['cancelled']} "
           f"timeouts {s1['timeouts'] - s0['timeouts']}", flush=True)
     print("  first 12 calls (us):", np.round(us[:12], 1).tolist(), flush=True)
+    if pipeline and os.environ.get("TILECAST_PIPE_TRACE") == "1":
+        g = C.c_int32()
+        N.lib().tc_debug_pipe_trace(None, 0, C.byref(g))
+        buf = np.zeros(64 * 3 * g.value, np.uint64)
+        N.lib().tc_debug_pipe_trace(buf.ctypes.data, buf.size, C.byref(g))
+        tr = buf.reshape(64, 3, g.value).astype(np.float64)
+        for k in range(1, 12):
+            a = tr[k]
+            ok = a[0] > 0
+            if not ok.any():
+                break
+            t0 = a[0][ok].min()
+            prev_end = tr[k - 1][2][tr[k - 1][2] > 0].max() if k else 0
+            print(f"  step {k}: gate spread {(a[0][ok].max() - t0) / 1e3:.2f} us, shipped "
+                  f"min/max +{(a[1][ok].min() - t0) / 1e3:.2f}/+{(a[1][ok].max() - t0) / 1e3:.2f} us, "
+                  f"frames min/med/max +{(a[2][ok].min() - t0) / 1e3:.2f}/"
+                  f"+{(np.median(a[2][ok]) - t0) / 1e3:.2f}/+{(a[2][ok].max() - t0) / 1e3:.2f} us, "
+                  f"gap after prev frames {(t0 - prev_end) / 1e3:.2f} us, "
+                  f"period {(t0 - tr[k - 1][0][tr[k - 1][0] > 0].min()) / 1e3:.2f} us", flush=True)
+    if pipeline:
+        print(f"  released steps: release call {split[0]:.1f} us, wait for results {split[1]:.1f} us "
+              f"({int(split[2])} steps); the rest is python", flush=True)
