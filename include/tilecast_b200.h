@@ -186,11 +186,12 @@ int tc_batch_step_into(const tc_spec *spec, const tc_state *state_in,
  * launches of the lean kernel chained per env instead of by a grid-wide
  * wait between them: state ping-pongs a -> b -> a ..., step k reads
  * actions_dev[k * n .. k * n + n) and writes outs[k % ring]; the final state
- * is in b when k_steps is odd, else in a. flags_dev: device u32[2 * n]
- * zeroed once per batch; epoch0: a per-batch counter the caller advances by
- * k_steps per call (epochs are never reused). One-wave batches: env i of
- * step k waits only for its own state from step k - 1 (and for the CTA of
- * the step that last wrote outs[k % ring]). Multi-wave batches (env
+ * is in b when k_steps is odd, else in a. flags_dev: device
+ * u32[n + max(n, 64 * 2048)] zeroed once per batch; epoch0: a per-batch
+ * counter the caller advances by k_steps per call (epochs are never reused).
+ * One-wave batches (rings of up to 64 blocks): env i of step k waits only
+ * for its own state from step k - 1 and for the CTA of the step that last
+ * wrote outs[k % ring] (a row of done epochs per ring slot). Multi-wave batches (env
  * tickets): env i of step k waits for env i's whole step k - 1; each launch
  * draws its tickets from its own slot of flags_dev[n ..), zeroed by a
  * stream-ordered memset per run of n launches. The first step waits for all

@@ -214,7 +214,10 @@ def batch_steps(bs: BatchState, actions: torch.Tensor, *, outs: Sequence[DeviceO
     sb = bs._retired[0] if bs._retired else DeviceState.alloc(bs.n, t.n_doors, t.n_entities,
                                                                bs.device)
     if not bs._chain:
-        bs._chain.extend([torch.zeros(2 * bs.n, dtype=torch.int32, device=bs.device), 1])
+        # [ready epochs u32[n] | one-wave done epochs, a row of 2048 per ring
+        # slot (<= 64) -- or the multi-wave ticket counters u32[n]]
+        bs._chain.extend([torch.zeros(bs.n + max(bs.n, 64 * 2048), dtype=torch.int32,
+                                      device=bs.device), 1])
     flags, epoch = bs._chain
     ring = (N.TcOut * len(outs))(*[o.c_struct() for o in outs])
     with torch.cuda.device(bs.device):

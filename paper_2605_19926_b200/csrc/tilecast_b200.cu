@@ -91,6 +91,8 @@ constexpr int WARPS_PER_CTA = 4;
 constexpr int BAND_BYTES_TARGET = 3072;       // per staging buffer
 constexpr int CTA_SCRATCH = 160;               // step kernel per-CTA scratch bytes
 constexpr int SMEM_MAP_MAX_CELLS = 4096;      // stage map in smem up to this
+constexpr int CHAIN_MAX_RING = 64;             // one wave: ring slots with done rows
+constexpr int CHAIN_DONE_ROW = 2048;           // done epochs per ring slot (>= CTAs)
 constexpr int CHAIN_MAX_WAVES = 4;            // tc_batch_steps chains multi-wave batches up to this
 constexpr int SMEM_U8_MAX_BYTES = 48 * 1024;  // u8 stop codes (+ tables) staged up to this
 
@@ -2830,6 +2832,11 @@ struct LeanSched {
   unsigned int* flags;
   unsigned int* tickets;
   unsigned int epoch, need_ready, need_done;
+  // one wave: the done epochs of the output block this launch writes are
+  // flags[done_off + cta] (one row per ring slot: launches that write other
+  // blocks may finish out of order, so a shared row would let a later
+  // launch's epoch stand in for the slot's previous writer)
+  unsigned int done_off;
   // Pipelined host step (tc_batch_step_pipelined): a launch made one step
   // ahead of its actions. After the previous grid (griddepcontrol.wait) and
   // the spec staging, CTA 0 polls the host gate words [go | cancel] (pinned,
@@ -3024,7 +3031,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
       // block this launch overwrites finished by the step that last wrote it
       if (lane == 0) {
         const volatile unsigned int* rd = ls.flags + i;
-        const volatile unsigned int* dn = ls.flags + n + blockIdx.x;
+        const volatile unsigned int* dn = ls.flags + ls.done_off + blockIdx.x;
         while ((int)(*rd - ls.need_ready) < 0 ||
                (ls.need_done != 0 && (int)(*dn - ls.need_done) < 0))
           __nanosleep(64);
@@ -3168,7 +3175,7 @@ lean_kernel(const __grid_constant__ SpecDev S, const __grid_constant__ StateDev 
     // every warp's frame writes are performed before the CTA's done epoch
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) *(volatile unsigned int*)(ls.flags + n + blockIdx.x) = ls.epoch;
+    if (threadIdx.x == 0) *(volatile unsigned int*)(ls.flags + ls.done_off + blockIdx.x) = ls.epoch;
   }
   // one wave: the mapped host step was released by ship_results as soon as
   // every env's reward / done had reached the host; nothing left to count
@@ -3995,6 +4002,7 @@ struct ChainArgs {
   unsigned int* flags;
   unsigned int* tickets;  // multi-wave: this launch's zeroed ticket counter
   unsigned int epoch, need_ready, need_done;
+  unsigned int done_off;  // one wave: this ring slot's row of done epochs
 };
 
 struct GateArgs {  // a pipelined (gated) launch, LeanSched::gate_*
@@ -4062,6 +4070,7 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
     ls.ctas = one_wave ? (int)((n + ls.epc - 1) / ls.epc) : 0;
     ls.flags = ls.tickets = nullptr;
     ls.epoch = ls.need_ready = ls.need_done = 0;
+    ls.done_off = 0;
     ls.gate_dev = gate ? gate->dev : nullptr;
     ls.gate_host = gate ? gate->host : nullptr;
     ls.gate_q = gate ? gate->q : 0u;
@@ -4077,6 +4086,7 @@ static int launch_batch_kernel(const tc_spec* s, const tc_state* state, const tc
       ls.epoch = chain->epoch;
       ls.need_ready = chain->need_ready;
       ls.need_done = one_wave ? chain->need_done : 0u;
+      ls.done_off = chain->done_off;
     }
     const long long* acts = reinterpret_cast<const long long*>(actions_dev);
     int ar = auto_reset, va = validate;
@@ -4147,7 +4157,9 @@ int tc_batch_steps(const tc_spec* s, const tc_state* state_a, const tc_state* st
   // its frame; at 2^20 envs, ~180 waves, the tail is < 1 % and the fences
   // cost ~20 %)
   const int64_t slots = lean2 ? (int64_t)s->lean16_ctas * lean_per_cta(s->dev.obs_w, false) : 0;
-  const bool chain_ok = !taps && (lean1 || (lean2 && n <= CHAIN_MAX_WAVES * slots));
+  // (one wave: a row of CHAIN_DONE_ROW done epochs per ring slot)
+  const bool chain_ok = !taps && ((lean1 && ring <= CHAIN_MAX_RING && s->lean_ctas <= CHAIN_DONE_ROW) ||
+                                  (lean2 && n <= CHAIN_MAX_WAVES * slots));
   // multi-wave: launch k draws env tickets from flags[n + k % n], zeroed
   // (stream-ordered after every earlier kernel) before each run of n launches
   uint32_t* const tickets = flags_dev + n;
@@ -4162,6 +4174,7 @@ int tc_batch_steps(const tc_spec* s, const tc_state* state_a, const tc_state* st
     // wraps, for the step that last wrote the output block it overwrites
     ca.need_ready = k == 0 ? 0u : ca.epoch - 1u;
     ca.need_done = (k >= ring) ? ca.epoch - (uint32_t)ring : 0u;
+    ca.done_off = (unsigned int)(n + (int64_t)(k % ring) * CHAIN_DONE_ROW);
     ca.tickets = tickets + (k % n);
     if (chain_ok && lean2 && k % n == 0) {
       const int64_t run = std::min<int64_t>(n, (int64_t)k_steps - k);
@@ -4565,6 +4578,14 @@ int tc_batch_step_pipelined(const tc_pipe_call* c) {
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
+  {
+    // the watchdog's clock for the launch waiting behind this step starts
+    // now, when the caller gets control back (a step longer than the
+    // timeout must not cancel its successor)
+    std::lock_guard<std::mutex> g2(P.mu);
+    if (P.pending.load(std::memory_order_relaxed) && P.key.flag == m.flag_host)
+      P.t_launch = host_us();
+  }
   // released steps: [3] release + bookkeeping, [4] wait for results, [5] count
   g_mapped_time[3] += t1 - t0;
   g_mapped_time[4] += host_us() - t1;

@@ -380,7 +380,10 @@ def test_zero_direction_reports_step_budget():
     ("my-way-home", 4096, 30, 3, False), ("key-door", 600, 25, 2, False),
     ("health-gathering", 1000, 20, 4, False), ("my-way-home", 20000, 6, 2, False),
     ("key-door", 16384, 12, 2, False), ("key-door", 9000, 10, 1, False),
-    ("dmlab-static-03@128", 8192, 6, 2, False), ("my-way-home", 4096, 6, 2, True)])
+    ("dmlab-static-03@128", 8192, 6, 2, False), ("my-way-home", 4096, 6, 2, True),
+    # far fewer CTAs than slots: many launches resident at once, finishing
+    # out of order (the per-slot done rows)
+    ("health-gathering", 256, 40, 3, False), ("key-door", 128, 40, 2, False)])
 def test_batch_steps_chained_equal_oracle(env, n, k, ring, taps):
     """tc.batch_steps: K step launches chained per env / CTA (no grid-wide
     wait between them) == K reference steps: the final state, the last

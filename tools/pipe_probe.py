@@ -17,7 +17,11 @@ from paper_2605_19926_b200 import _native as N  # noqa: E402
 env = sys.argv[1] if len(sys.argv) > 1 else "my-way-home"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 K = int(sys.argv[3]) if len(sys.argv) > 3 else 300
-spec = tc.make_env(env)
+if env in ("c2", "c3", "c4", "c5", "large"):  # a bench config's spec
+    import bench
+    spec = bench.make_spec(env)
+else:
+    spec = tc.make_env(env)
 acts = tc.policy_actions(spec, n, K + 5, 1)
 for pipeline in (False, True):
     bs = tc.batch_reset(spec, n, 1)
