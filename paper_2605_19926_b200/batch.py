@@ -153,6 +153,17 @@ class _ActionStage:
         self.fn = None  # cached ctypes entry point of batch_step_host
         self.dev_index = torch.device(device).index
 
+    def __del__(self):
+        # a pipelined step launched by this stage may still be waiting at its
+        # gate in this stage's pinned words: cancel it and let it exit before
+        # the pinned / device buffers go back to torch's allocators
+        try:
+            if N.pipe_stats()["pending"]:
+                N.pipe_cancel()
+                torch.cuda.synchronize(self.dev_index)
+        except Exception:
+            pass
+
     def next_buffer(self) -> np.ndarray:
         """The next pinned buffer, once the H2D copy that last read it is done."""
         self.k ^= 1
