@@ -46,11 +46,14 @@ for s in range(K):
     float(r.sum())
 t1 = time.perf_counter()
 print(f"reward sum {1e6*(t1-t0)/K:.2f} us")
+# the native pipelined call alone, with pipelining off (one launch per call)
 key = next(iter(stg.calls))
-args = stg.calls[key][0]
+cs = stg.calls[key][1]
+cs.speculate = 0
 stg.fn = real
+tc.pipeline_drain()
 t0 = time.perf_counter()
 for s in range(K):
-    real(*args)
+    real(stg.calls[key][0])
 t1 = time.perf_counter()
-print(f"native mapped call {1e6*(t1-t0)/K:.1f} us")
+print(f"native step call (not pipelined) {1e6*(t1-t0)/K:.1f} us")

@@ -1,5 +1,7 @@
-"""Host-side split of the mapped host step (batch_step_host) at C2: Python
-around the call, the launch call, the wait for the kernel's completion word."""
+"""Host-side split of the non-pipelined mapped host step (batch_step_host
+with pipeline=False) at C2: Python around the call, the launch call, the
+wait for the kernel's completion word. tools/pipe_probe.py covers the
+pipelined step."""
 import ctypes as C
 import sys
 import time
@@ -18,7 +20,7 @@ n, K = 4096, 400
 acts = tc.policy_actions(spec, n, K + 5, 1)
 bs = tc.batch_reset(spec, n, 1)
 for s in range(5):
-    bs, r, d = tc.batch_step_host(bs, acts[s], reuse=True)
+    bs, r, d = tc.batch_step_host(bs, acts[s], reuse=True, pipeline=False)
 torch.cuda.synchronize()
 lib = N.lib()
 lib.tc_debug_mapped_timing.argtypes = [C.c_void_p, C.c_int32]
@@ -26,7 +28,7 @@ out = np.zeros(3)
 lib.tc_debug_mapped_timing(out.ctypes.data, 1)
 t0 = time.perf_counter()
 for s in range(K):
-    bs, r, d = tc.batch_step_host(bs, acts[5 + s], reuse=True)
+    bs, r, d = tc.batch_step_host(bs, acts[5 + s], reuse=True, pipeline=False)
 torch.cuda.synchronize()
 el = (time.perf_counter() - t0) / K * 1e6
 lib.tc_debug_mapped_timing(out.ctypes.data, 1)
